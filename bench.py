@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the Parallel Space Saving hot path on B200 (one JSON line on rank 0).
+
+A step is one pass of the whole hot path over the workload:
+pss_summarize (K1) -> pss_merge (K2) -> pss_prune (K3) -> pss_verify (K4) -> pss_report (K5),
+all through the C-ABI of libpss.so, inputs resident in HBM. Default workload: the metric's
+configuration (BASELINE.json "metric": n = 2^29 uint32 Zipf(1.1), k = 1000), P = 8192.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload H] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL): every rank owns an equal shard of one
+longer stream (weak scaling); the rank-local subtree roots are all-gathered and the top levels of
+the same fixed tree are finished on every rank, then exact counts are all-reduced
+(paper_1606_04669_b200/dist.py). `--impl reference` times the CPU oracle instead (the reference
+arm of this tier): a bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gitems/s for summarize+merge (and verify) at n=2^29, k=1000; % of HBM roofline"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="H")
+    ap.add_argument("--P", type=int, default=0, help="override the number of partitions")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ helpers
+def host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy kernel, read+write)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch of K1 from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(workload, {}).get("summarize_dram_bytes_per_launch")
+    return float(v) if v is not None else None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------ oracle arms
+def oracle_sample(w, seconds: float, threads: int, A_host=None):
+    """Time the oracle, as it stands, on the first S blocks of the workload (S sized so one run
+    takes about `seconds`). Returns (items/s, description, threads)."""
+    import numpy as np
+
+    import inputs
+    import oracle
+
+    chunk = w.n // w.P
+    A1 = A_host[:chunk] if A_host is not None else w.generate(chunk)
+    t0 = time.perf_counter()
+    oracle.space_saving(A1, w.k)
+    t1 = max(time.perf_counter() - t0, 1e-4)
+    S = int(max(1, min(w.P, threads * max(1, math.floor(seconds * 0.8 / t1)))))
+    S = 1 << int(math.log2(S)) if S > 1 else 1
+    m = S * chunk
+    A = A_host[:m] if A_host is not None else w.generate(m)
+    t0 = time.perf_counter()
+    pl = oracle.pipeline(np.ascontiguousarray(A), w.k, S, threads=threads)
+    dt = time.perf_counter() - t0
+    desc = (f"first {S} of {w.P} blocks ({m} keys, {100.0 * m / w.n:.2f}% of n), k={w.k}: "
+            f"leaves + fixed tree + prune + verify + report, oracle/pss_oracle.c via ctypes, "
+            f"leaves on {threads} threads")
+    del pl
+    return m / dt, desc, threads, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on this box's host cores (the tier's reference arm)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import inputs
+
+    w = inputs.WORKLOADS[args.workload]
+    T = host_threads()
+    budget = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    chunk = w.n // w.P
+    rates = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        rate, desc, cores, dt = oracle_sample(w, budget, T)
+        if i >= args.warmup:
+            rates.append(rate)
+    v = statistics.median(rates) / 1e9
+    line = {"metric": METRIC, "value": v, "unit": "Gitems/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w),
+            "data": "synthetic", "impl": "reference",
+            "config": config_of(w, w.P, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "Gitems/s", "cores": T, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": "Gitems/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def dtype_of(w):
+    return "u32" if w.key_bytes == 4 else "u64"
+
+
+def config_of(w, P, gpus):
+    d = w.describe()
+    d["P"] = P
+    d["global_n"] = w.n * gpus
+    d["parallelism"] = f"dp{gpus}" if gpus > 1 else "1gpu"
+    d["l2"] = (f"inputs larger than L2 ({w.n * w.key_bytes / 2**30:.1f} GiB/GPU streamed per pass "
+               f"vs 126 MB L2), no flush needed")
+    return d
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+
+    import inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+
+    import paper_1606_04669_b200 as pss
+    from paper_1606_04669_b200 import dist as pdist
+
+    w = inputs.WORKLOADS[args.workload]
+    n, k = w.n, w.k
+    P = args.P or w.P
+    kb = w.key_bytes
+    kt = pss.KEY_U32 if kb == 4 else pss.KEY_U64
+
+    # this rank's shard: positions [rank*n, (rank+1)*n) of one stream (weak scaling)
+    h_A = torch.empty((n,), dtype=torch.uint32 if kb == 4 else torch.uint64, pin_memory=True)
+    w.generate(n, out=h_A.numpy(), start=rank * n)
+    d_A = h_A.to(dev)
+
+    runner = pdist.Runner(n, k, P, kt, dev, world=world, rank=rank, group=pg)
+    stream = torch.cuda.current_stream()
+
+    def step(A, ev=None):
+        return runner.step(A, ev)
+
+    for _ in range(args.warmup):
+        step(d_A)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if pg is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(K):
+            step(d_A, evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if pg is not None:
+        torch.distributed.barrier()
+    ms = t_start.elapsed_time(t_end)
+    per = {"summarize": [], "merge": [], "tail": []}
+    for e in evs:
+        per["summarize"].append(e[0].elapsed_time(e[1]))
+        per["merge"].append(e[1].elapsed_time(e[2]))
+        per["tail"].append(e[2].elapsed_time(e[3]))
+    if pg is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / K
+    value = world * n / (ms_step * 1e-3) / 1e9
+
+    # correctness of the last step against a brute-force-free invariant: the answer is sorted
+    # and every reported count reaches the threshold (full parity lives in tests/)
+    res_items, res_counts, res_len = runner.result()
+    ln = int(res_len.item())
+    thr = world * n // k + 1
+    counts = res_counts[:ln].cpu().numpy()
+    assert (counts >= thr).all() and (np.diff(counts.astype(np.int64)) <= 0).all()
+
+    # ---- end to end: host (pinned) keys -> H2D -> path -> D2H of the answer, every step
+    E = args.e2e_steps or min(K, 5)
+    e2e_ms = []
+    for i in range(E + 1):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        if pg is not None:
+            torch.distributed.barrier()
+        a.record(stream)
+        out = runner.step_host(h_A, d_A)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i > 0:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e = statistics.median(e2e_ms)
+    if pg is not None:
+        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+    h2d = n * kb
+    d2h = k * kb + k * 8 + 4
+
+    # ---- roofline of the dominant kernel (K1 summarize): algorithmic bytes = n * key bytes
+    peak, peak_src = measured_peaks()
+    t_k1 = statistics.mean(per["summarize"])  # ms per launch, CUDA events on its stream
+    achieved = n * kb / (t_k1 * 1e-3) / 1e9
+    traffic = ncu_traffic(args.workload)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "ss_summarize_kernel",
+            "algorithmic_bytes_per_launch": n * kb, "peak_source": peak_src,
+            "ms_per_launch": round(t_k1, 4)}
+
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "Gitems/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w),
+            "data": "synthetic", "config": config_of(w, P, world),
+            "phases_ms": {p: round(statistics.mean(v), 4) for p, v in per.items()},
+            "summarize_merge_gitems_s": round(
+                n / ((statistics.mean(per["summarize"]) + statistics.mean(per["merge"])) * 1e-3) / 1e9, 3),
+            "hbm_frac_of_8TBs_summarize_merge": round(
+                n * kb / ((statistics.mean(per["summarize"]) + statistics.mean(per["merge"])) * 1e-3) / 8e12, 4),
+            "roofline": roof,
+            "e2e": {"value": round(world * n / (e2e * 1e-3) / 1e9, 3), "unit": "Gitems/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": round(e2e, 3), "api": runner.host_api},
+            "gpu_launches": runner.launches_per_step * K,
+            "clocks": clk.summary(),
+            "result_len": ln}
+    if world == 1 and not args.no_cpu_baseline:
+        rate, desc, cores, dt = oracle_sample(w, args.cpu_seconds, host_threads(), h_A.numpy())
+        line["cpu_baseline"] = {"value": round(rate / 1e9, 6), "unit": "Gitems/s", "cores": cores,
+                                "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/*
+ * pss.h -- C-ABI of libpss.so: the data-parallel hot path of Parallel Space Saving
+ * (Cafaro, Pulimeno, Epicoco, Aloisio, "Parallel Space Saving on Multi and Many-Core Processors",
+ * arXiv 1606.04669) on one NVIDIA B200 (sm_100a).
+ *
+ * Citations "P:line" are lines of the paper's text; readings R1..R12 of points the paper
+ * leaves open are listed in DESIGN.md section 3 and apply to every call below.
+ *
+ * Conventions shared by every call
+ *  - Memory: every pointer named d_* and every pointer inside pss_summaries is DEVICE memory owned
+ *    by the caller (e.g. torch tensors); h_* pointers are HOST memory (pinned recommended). The
+ *    library never allocates or frees memory and keeps no global mutable state.
+ *  - Asynchrony: every call enqueues work on `stream` and returns; outputs are valid after the
+ *    stream is synchronised. Calls on distinct streams may run concurrently if their buffers and
+ *    workspaces are disjoint.
+ *  - Errors: arguments are validated before anything is launched; a failed validation returns a
+ *    status != PSS_OK and launches nothing. A launch failure returns PSS_ERR_CUDA (the CUDA error is
+ *    read with cudaGetLastError). No exception crosses the ABI.
+ *  - Keys: uint32 or uint64 item ids (pss_key_type). Every value, including 0 and all-ones, is a
+ *    valid id (R12). Counts and errors are uint32 (R9: n <= 2^31 so f_hat <= n + n/k < 2^32);
+ *    exact counts are uint64.
+ *  - Workspace: scratch device memory of at least pss_workspace_bytes(op, ...) bytes, 256-byte
+ *    aligned, passed as d_ws/ws_bytes; its contents need not be initialised and are clobbered.
+ */
+#ifndef PSS_H_
+#define PSS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef __CUDA_RUNTIME_API_H__
+typedef struct CUstream_st* cudaStream_t;
+#endif
+
+typedef enum {
+  PSS_OK = 0,
+  PSS_ERR_INVALID_ARG = 1,         /* null pointer, k < 2, P == 0, bad key type, ... */
+  PSS_ERR_UNSUPPORTED = 2,         /* n > 2^31 (u32 counters, R9), k > PSS_MAX_K */
+  PSS_ERR_CAPACITY_MISMATCH = 3,   /* summaries with different k or key type */
+  PSS_ERR_WORKSPACE_TOO_SMALL = 4, /* ws_bytes < pss_workspace_bytes(...) */
+  PSS_ERR_CUDA = 5                 /* a CUDA launch or runtime call failed */
+} pss_status;
+
+typedef enum { PSS_KEY_U32 = 0, PSS_KEY_U64 = 1 } pss_key_type;
+
+/* ops for pss_workspace_bytes */
+typedef enum {
+  PSS_OP_SUMMARIZE = 0,
+  PSS_OP_MERGE = 1,
+  PSS_OP_COMBINE = 2,
+  PSS_OP_VERIFY = 3,
+  PSS_OP_QUERY = 4
+} pss_op;
+
+#define PSS_MAX_K 65000u
+#define PSS_MAX_N (1ull << 31)
+
+/*
+ * A batch of `count` stream summaries of capacity k, structure of arrays, in device memory.
+ * Summary i occupies entries [i*k, i*k + sizes[i]) of items/counts/errs; entries past sizes[i] are
+ * unspecified. A counter is (item e, estimated frequency f_hat, error eps) (eps is reading
+ * R3 -- the paper's summaries store (e, f_hat) only). Leaves are in slot order (R2); merged
+ * summaries and roots are in canonical order: count descending, then item ascending (R5).
+ */
+typedef struct {
+  int32_t key_type;  /* pss_key_type */
+  uint32_t k;        /* counters per summary, 2 <= k <= PSS_MAX_K */
+  uint32_t count;    /* number of summaries */
+  void* items;       /* [count][k] uint32_t or uint64_t */
+  uint32_t* counts;  /* [count][k] f_hat */
+  uint32_t* errs;    /* [count][k] eps */
+  uint32_t* sizes;   /* [count] occupied counters, <= k */
+} pss_summaries;
+
+/* Bytes of workspace an op needs. For PSS_OP_VERIFY, k is the candidate capacity (max n_cand);
+ * for PSS_OP_MERGE, P is the number of leaves; n is ignored except by SUMMARIZE and QUERY. */
+size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_type kt);
+
+/*
+ * pss_summarize -- the per-block local step of Algorithm 1: block decomposition
+ * left = floor(r n / P), right = floor((r+1) n / P) - 1 for r = 0..P-1 (Alg. 1 l.3-4, P:92-95;
+ * P:84), then SpaceSaving(A, left, right, k) on every block (Alg. 1 l.5; update
+ * rules P:82 with R1: ties evict the lowest slot index; R2: free counters fill in slot order).
+ *   d_A     : n keys of type kt, read-only, naturally aligned.
+ *   n       : 0 <= n <= 2^31.
+ *   k, P    : k >= 2 ("2 <= k"; k > n is allowed and gives exact summaries); P >= 1
+ *             (P > n gives empty leaves, R10).
+ *   leaves  : caller-owned, leaves->count == P, leaves->k == k, leaves->key_type == kt. Written:
+ *             sizes[r] and entries [r*k, r*k + sizes[r]) in slot order.
+ */
+pss_status pss_summarize(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, uint32_t P,
+                         pss_summaries* leaves, void* d_ws, size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_merge -- ParallelReduction(local, k, COMBINE) (Alg. 1 l.7) over a fixed balanced
+ * binary tree (R6): level by level, nodes (2i, 2i+1) are combined with COMBINE (Alg. 2,
+ * P:122-157) and an odd last node is carried up unchanged. COMBINE is commutative but not
+ * associative, so the tree shape is part of the result.
+ *   leaves : P = leaves->count >= 1 summaries (any order within a summary).
+ *   root   : root->count == 1, same k and key type. Written in canonical order (R5).
+ */
+pss_status pss_merge(const pss_summaries* leaves, pss_summaries* root, void* d_ws,
+                     size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_combine -- one COMBINE(S1, S2, k) (Alg. 2; prose P:112-115) for every i:
+ * out[i] = COMBINE(a[i], b[i]). m1, m2 are the minima of S1, S2 (0 for a summary with fewer than
+ * k occupied counters, R4); matched items get f1 + f2 (eps1 + eps2), items of S1 only f1 + m2
+ * (eps1 + m2), items of S2 only f2 + m1 (eps2 + m1); Prune(k) keeps the k greatest (R5 ties).
+ *   a, b, out : same k and key type; a->count == b->count == out->count.
+ */
+pss_status pss_combine(const pss_summaries* a, const pss_summaries* b, pss_summaries* out,
+                       void* d_ws, size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_prune -- Pruned(global, n, k) (Alg. 1 l.8-9): keep the root counters with
+ * f_hat >= floor(n/k) + 1 (the k-majority threshold; R7), in root order.
+ *   root     : one summary in canonical order (as written by pss_merge).
+ *   d_cand   : capacity root->k keys of the root's type; d_n_cand : one uint32.
+ */
+pss_status pss_prune(const pss_summaries* root, uint64_t n, void* d_cand, uint32_t* d_n_cand,
+                     cudaStream_t stream);
+
+/*
+ * pss_verify -- the off-line verification scan ("a parallel scan of the input can be used to
+ * determine the actual frequent items"): d_exact[j] = #{i < n : A[i] == cand[j]} (R8).
+ *   d_cand   : n_cand keys (duplicates allowed).
+ *   d_n_cand : optional (may be NULL) device uint32 holding the actual number of candidates; the
+ *              kernels use min(*d_n_cand, n_cand), so the call can follow pss_prune without a host
+ *              round trip. Entries of d_exact past that count are left untouched.
+ *   d_exact  : n_cand uint64 outputs, candidate order.
+ */
+pss_status pss_verify(const void* d_A, uint64_t n, pss_key_type kt, const void* d_cand,
+                      uint32_t n_cand, const uint32_t* d_n_cand, uint64_t* d_exact, void* d_ws,
+                      size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_report -- the k-majority answer after verification: the candidates whose exact
+ * count reaches floor(n/k) + 1, ordered by (exact count desc, item asc). The candidates must be
+ * distinct (as written by pss_prune).
+ *   d_cand, n_cand, d_n_cand : as for pss_verify; d_exact : their exact counts.
+ *   d_out_items : capacity n_cand keys; d_out_counts : capacity n_cand uint64; d_out_len : uint32.
+ */
+pss_status pss_report(const void* d_cand, uint32_t n_cand, const uint32_t* d_n_cand,
+                      const uint64_t* d_exact, pss_key_type kt, uint64_t n, uint32_t k,
+                      void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                      cudaStream_t stream);
+
+/*
+ * pss_query -- the whole off-line pipeline: summarize, merge, prune, verify, then report the
+ * k-majority set {(x, f(x)) : f(x) >= floor(n/k) + 1} ordered by (f desc, x asc).
+ * Exact by the no-false-negative guarantee plus verification.
+ *   d_out_items  : capacity k keys; d_out_counts : capacity k uint64; d_out_len : one uint32.
+ */
+pss_status pss_query(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, uint32_t P,
+                     void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len, void* d_ws,
+                     size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_query_host -- pss_query from HOST buffers (the end-to-end call): copies h_A (n keys,
+ * host, pinned recommended) to d_A (device, capacity n keys), runs pss_query, and copies the
+ * result back to h_out_items (capacity k), h_out_counts (capacity k) and h_out_len (one uint32).
+ * The d->h copies are enqueued on `stream`; the host buffers are valid after it is synchronised.
+ */
+pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                          uint32_t P, void* h_out_items, uint64_t* h_out_counts,
+                          uint32_t* h_out_len, void* d_ws, size_t ws_bytes, cudaStream_t stream);
+
+/* Human-readable name of a status. */
+const char* pss_status_string(pss_status s);
+
+/* Library version, e.g. "pss-b200 0.1". */
+const char* pss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSS_H_ */

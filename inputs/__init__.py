@@ -40,6 +40,11 @@ def _load():
         lib.pssgen_zipf.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
                                     ctypes.c_int]
+        lib.pssgen_zipf_range.restype = ctypes.c_int
+        lib.pssgen_zipf_range.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
+                                          ctypes.c_int]
         lib.pssgen_mix32.restype = ctypes.c_uint32
         lib.pssgen_mix32.argtypes = [ctypes.c_uint32]
         lib.pssgen_mix64.restype = ctypes.c_uint64
@@ -57,18 +62,17 @@ def host_threads() -> int:
 
 def zipf(n: int, s: float, universe: float, seed: int, key_bytes: int = 4,
          tail_frac: float = 0.0, hash_ids: bool = True, threads: int | None = None,
-         out: np.ndarray | None = None) -> np.ndarray:
-    """n i.i.d. Zipf(s) keys over `universe` ranks (hashed ids), as a numpy u32/u64 array.
-
-    `out` may be a preallocated (e.g. pinned) contiguous array of the right dtype and size.
+         out: np.ndarray | None = None, start: int = 0) -> np.ndarray:
+    """Positions [start, start + n) of the i.i.d. Zipf(s) stream over `universe` ranks (hashed
+    ids), as a numpy u32/u64 array. `out` may be a preallocated (e.g. pinned) contiguous array.
     """
     dt = np.uint32 if key_bytes == 4 else np.uint64
     if out is None:
         out = np.empty(int(n), dtype=dt)
     assert out.dtype == dt and out.size == n and out.flags["C_CONTIGUOUS"]
-    rc = _load().pssgen_zipf(out.ctypes.data if n else None, int(n), key_bytes, float(s),
-                             float(universe), int(seed), float(tail_frac), int(hash_ids),
-                             int(threads or host_threads()))
+    rc = _load().pssgen_zipf_range(out.ctypes.data if n else None, int(start), int(n), key_bytes,
+                                   float(s), float(universe), int(seed), float(tail_frac),
+                                   int(hash_ids), int(threads or host_threads()))
     if rc != 0:
         raise ValueError("pssgen_zipf rejected its arguments")
     return out
@@ -97,10 +101,10 @@ class Workload:
     verify: bool = True
     note: str = field(default="", compare=False)
 
-    def generate(self, n: int | None = None, out=None, threads=None) -> np.ndarray:
-        """The first `n` (default all) keys of this workload (a prefix is the same stream)."""
+    def generate(self, n: int | None = None, out=None, threads=None, start: int = 0) -> np.ndarray:
+        """Keys [start, start + n) (default: the whole workload) of this workload's stream."""
         return zipf(self.n if n is None else n, self.s, self.universe, self.seed, self.key_bytes,
-                    self.tail_frac, True, threads, out)
+                    self.tail_frac, True, threads, out, start)
 
     def describe(self) -> dict:
         return {"workload": self.name, "n": self.n, "key": "u32" if self.key_bytes == 4 else "u64",

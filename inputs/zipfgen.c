@@ -102,6 +102,7 @@ static uint64_t zipf_sample(const zipf_t* z, uint64_t seed, uint64_t i, uint32_t
 
 typedef struct {
   void* out;
+  uint64_t offset; /* global position of out[0] */
   uint64_t begin, end;
   int key_bytes;
   double s;
@@ -124,17 +125,18 @@ static void* worker(void* arg) {
     }
     if (jb->key_bytes == 4) {
       uint32_t r = (uint32_t)rank;
-      ((uint32_t*)jb->out)[i] = jb->hash_ids ? fmix32(r) : r;
+      ((uint32_t*)jb->out)[i - jb->offset] = jb->hash_ids ? fmix32(r) : r;
     } else {
-      ((uint64_t*)jb->out)[i] = jb->hash_ids ? fmix64(rank) : rank;
+      ((uint64_t*)jb->out)[i - jb->offset] = jb->hash_ids ? fmix64(rank) : rank;
     }
   }
   return NULL;
 }
 
-/* Fill out[0..n) with Zipf(s) keys over universe U (see header). Returns 0 on success. */
-int pssgen_zipf(void* out, uint64_t n, int key_bytes, double s, double U, uint64_t seed,
-                double tail_frac, int hash_ids, int nthreads) {
+/* Fill out[0..n) with positions [start, start + n) of the Zipf(s) stream over universe U (see
+ * header); a range of the stream is identical to the same positions of a longer stream. */
+int pssgen_zipf_range(void* out, uint64_t start, uint64_t n, int key_bytes, double s, double U,
+                      uint64_t seed, double tail_frac, int hash_ids, int nthreads) {
   if (!out && n) return -1;
   if (key_bytes != 4 && key_bytes != 8) return -1;
   if (!(s > 0.0) || !(U >= 1.0)) return -1;
@@ -144,11 +146,17 @@ int pssgen_zipf(void* out, uint64_t n, int key_bytes, double s, double U, uint64
   pthread_t th[256];
   job_t jobs[256];
   for (int t = 0; t < nthreads; ++t) {
-    jobs[t] = (job_t){out, n * (uint64_t)t / nthreads, n * (uint64_t)(t + 1) / nthreads, key_bytes,
-                      s, U, seed, tail_frac, hash_ids};
+    jobs[t] = (job_t){out, start, start + n * (uint64_t)t / nthreads,
+                      start + n * (uint64_t)(t + 1) / nthreads, key_bytes, s, U, seed, tail_frac,
+                      hash_ids};
   }
   for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, worker, &jobs[t]);
   worker(&jobs[0]);
   for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
   return 0;
+}
+
+int pssgen_zipf(void* out, uint64_t n, int key_bytes, double s, double U, uint64_t seed,
+                double tail_frac, int hash_ids, int nthreads) {
+  return pssgen_zipf_range(out, 0, n, key_bytes, s, U, seed, tail_frac, hash_ids, nthreads);
 }

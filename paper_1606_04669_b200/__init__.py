@@ -1,0 +1,277 @@
+"""pss-b200: the data-parallel hot path of Parallel Space Saving (arXiv 1606.04669) on one B200.
+
+A thin Python binding over the C-ABI library ``libpss.so`` (include/pss.h). Every function here
+only marshals arguments: tensors are passed as device pointers, the current torch stream as the
+CUDA stream, and every step of the method runs in the CUDA kernels of ``csrc/``. There is no CPU
+fallback: importing this package fails loudly if ``libpss.so`` has not been built
+(``python -c "import __graft_entry__ as g; g.build()"``).
+
+Names mirror the C functions: pss_summarize, pss_merge, pss_combine, pss_prune, pss_verify,
+pss_query, pss_query_host, pss_workspace_bytes.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = ["Summaries", "PssError", "pss_workspace_bytes", "pss_summarize", "pss_merge",
+           "pss_combine", "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host", "lib_path",
+           "KEY_U32", "KEY_U64", "OP_SUMMARIZE", "OP_MERGE", "OP_COMBINE", "OP_VERIFY", "OP_QUERY",
+           "EXPORTED_SYMBOLS"]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "libpss.so")
+
+KEY_U32, KEY_U64 = 0, 1
+OP_SUMMARIZE, OP_MERGE, OP_COMBINE, OP_VERIFY, OP_QUERY = range(5)
+STATUS = {0: "PSS_OK", 1: "PSS_ERR_INVALID_ARG", 2: "PSS_ERR_UNSUPPORTED",
+          3: "PSS_ERR_CAPACITY_MISMATCH", 4: "PSS_ERR_WORKSPACE_TOO_SMALL", 5: "PSS_ERR_CUDA"}
+EXPORTED_SYMBOLS = ["pss_workspace_bytes", "pss_summarize", "pss_merge", "pss_combine",
+                    "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host",
+                    "pss_status_string", "pss_version"]
+
+
+class PssError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        super().__init__(f"{fn} returned {STATUS.get(status, status)}")
+        self.status = status
+
+
+class _Summ(ctypes.Structure):
+    _fields_ = [("key_type", ctypes.c_int32), ("k", ctypes.c_uint32), ("count", ctypes.c_uint32),
+                ("items", ctypes.c_void_p), ("counts", ctypes.c_void_p), ("errs", ctypes.c_void_p),
+                ("sizes", ctypes.c_void_p)]
+
+
+if not os.path.exists(lib_path):
+    raise ImportError(f"{lib_path} is missing: build it first (__graft_entry__.build()); "
+                      "there is no CPU fallback")
+_lib = ctypes.CDLL(lib_path)
+_vp, _u64, _u32, _i32, _sz = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
+                              ctypes.c_size_t)
+_SP = ctypes.POINTER(_Summ)
+_lib.pss_workspace_bytes.argtypes = [_i32, _u64, _u32, _u32, _i32]
+_lib.pss_workspace_bytes.restype = _sz
+_lib.pss_summarize.argtypes = [_vp, _u64, _i32, _u32, _u32, _SP, _vp, _sz, _vp]
+_lib.pss_merge.argtypes = [_SP, _SP, _vp, _sz, _vp]
+_lib.pss_combine.argtypes = [_SP, _SP, _SP, _vp, _sz, _vp]
+_lib.pss_prune.argtypes = [_SP, _u64, _vp, _vp, _vp]
+_lib.pss_verify.argtypes = [_vp, _u64, _i32, _vp, _u32, _vp, _vp, _vp, _sz, _vp]
+_lib.pss_report.argtypes = [_vp, _u32, _vp, _vp, _i32, _u64, _u32, _vp, _vp, _vp, _vp]
+_lib.pss_query.argtypes = [_vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
+_lib.pss_query_host.argtypes = [_vp, _vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
+for _f in ("pss_summarize", "pss_merge", "pss_combine", "pss_prune", "pss_verify", "pss_report",
+           "pss_query", "pss_query_host"):
+    getattr(_lib, _f).restype = _i32
+_lib.pss_status_string.argtypes = [_i32]
+_lib.pss_status_string.restype = ctypes.c_char_p
+_lib.pss_version.restype = ctypes.c_char_p
+
+
+def version() -> str:
+    return _lib.pss_version().decode()
+
+
+def _check(fn: str, st: int):
+    if st != 0:
+        raise PssError(fn, st)
+
+
+def _key_type(t: torch.Tensor) -> int:
+    if t.dtype in (torch.uint32, torch.int32):
+        return KEY_U32
+    if t.dtype in (torch.uint64, torch.int64):
+        return KEY_U64
+    raise TypeError(f"keys must be uint32/uint64 (or int32/int64 bit patterns), got {t.dtype}")
+
+
+def _key_dtype(kt: int):
+    return torch.uint32 if kt == KEY_U32 else torch.uint64
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev_keys(A: torch.Tensor) -> torch.Tensor:
+    if not A.is_cuda:
+        raise ValueError("A must be a CUDA tensor (use pss_query_host for host buffers)")
+    if not A.is_contiguous():
+        raise ValueError("A must be contiguous")
+    return A
+
+
+def _ws(nbytes: int, ws: torch.Tensor | None, device) -> torch.Tensor:
+    if ws is not None and ws.numel() * ws.element_size() >= nbytes:
+        return ws.view(torch.uint8) if ws.dtype != torch.uint8 else ws
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def pss_workspace_bytes(op: int, n: int, k: int, P: int, key_type: int) -> int:
+    return int(_lib.pss_workspace_bytes(op, n, k, P, key_type))
+
+
+@dataclass
+class Summaries:
+    """`count` summaries of capacity k (device tensors, structure of arrays; include/pss.h)."""
+    items: torch.Tensor   # [count, k] uint32|uint64
+    counts: torch.Tensor  # [count, k] uint32
+    errs: torch.Tensor    # [count, k] uint32
+    sizes: torch.Tensor   # [count] uint32
+
+    @staticmethod
+    def empty(count: int, k: int, key_type: int, device="cuda") -> "Summaries":
+        return Summaries(torch.empty((count, k), dtype=_key_dtype(key_type), device=device),
+                         torch.empty((count, k), dtype=torch.uint32, device=device),
+                         torch.empty((count, k), dtype=torch.uint32, device=device),
+                         torch.zeros((count,), dtype=torch.uint32, device=device))
+
+    @property
+    def k(self) -> int:
+        return int(self.items.shape[1])
+
+    @property
+    def count(self) -> int:
+        return int(self.items.shape[0])
+
+    @property
+    def key_type(self) -> int:
+        return _key_type(self.items)
+
+    def _c(self) -> _Summ:
+        return _Summ(self.key_type, self.k, self.count, self.items.data_ptr(),
+                     self.counts.data_ptr(), self.errs.data_ptr(), self.sizes.data_ptr())
+
+    def host(self, i: int = 0):
+        """Summary i as host lists [(item, count, err)] (items as unsigned ints)."""
+        n = int(self.sizes[i].item())
+        it = self.items[i, :n].cpu().numpy().astype("uint64").tolist()
+        c = self.counts[i, :n].cpu().numpy().astype("uint64").tolist()
+        e = self.errs[i, :n].cpu().numpy().astype("uint64").tolist()
+        return list(zip(it, c, e))
+
+
+def pss_summarize(A: torch.Tensor, k: int, P: int, out: Summaries | None = None,
+                  workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """Per-block Space Saving leaves (Alg. 1 l.3-5): see include/pss.h."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    out = out or Summaries.empty(P, k, kt, A.device)
+    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE, A.numel(), k, P, kt), workspace, A.device)
+    c = out._c()
+    _check("pss_summarize", _lib.pss_summarize(A.data_ptr(), A.numel(), kt, k, P, ctypes.byref(c),
+                                               ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
+def pss_merge(leaves: Summaries, out: Summaries | None = None,
+              workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """Fixed binary COMBINE tree over the leaves (Alg. 1 l.7, Alg. 2) -> root (canonical)."""
+    out = out or Summaries.empty(1, leaves.k, leaves.key_type, leaves.items.device)
+    ws = _ws(pss_workspace_bytes(OP_MERGE, 0, leaves.k, leaves.count, leaves.key_type), workspace,
+             leaves.items.device)
+    a, b = leaves._c(), out._c()
+    _check("pss_merge", _lib.pss_merge(ctypes.byref(a), ctypes.byref(b), ws.data_ptr(), ws.numel(),
+                                       _stream(stream)))
+    return out
+
+
+def pss_combine(a: Summaries, b: Summaries, out: Summaries | None = None,
+                workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """out[i] = COMBINE(a[i], b[i]) (Alg. 2), canonical order."""
+    out = out or Summaries.empty(a.count, a.k, a.key_type, a.items.device)
+    ws = _ws(pss_workspace_bytes(OP_COMBINE, 0, a.k, a.count, a.key_type), workspace, a.items.device)
+    ca, cb, co = a._c(), b._c(), out._c()
+    _check("pss_combine", _lib.pss_combine(ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co),
+                                           ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
+def pss_prune(root: Summaries, n: int, stream=None):
+    """Pruned(global, n, k) (Alg. 1 l.8-9): (candidates[k] device keys, n_cand[1] device uint32)."""
+    cand = torch.empty((root.k,), dtype=root.items.dtype, device=root.items.device)
+    n_cand = torch.zeros((1,), dtype=torch.uint32, device=root.items.device)
+    c = root._c()
+    _check("pss_prune", _lib.pss_prune(ctypes.byref(c), n, cand.data_ptr(), n_cand.data_ptr(),
+                                       _stream(stream)))
+    return cand, n_cand
+
+
+def pss_verify(A: torch.Tensor, cand: torch.Tensor, n_cand: torch.Tensor | None = None,
+               out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """Exact counts of the candidates over A. Returns uint64[len(cand)] on the device."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    if _key_type(cand) != kt:
+        raise TypeError("candidate and key types differ")
+    cap = cand.numel()
+    out = out if out is not None else torch.zeros((max(cap, 1),), dtype=torch.uint64, device=A.device)
+    ws = _ws(pss_workspace_bytes(OP_VERIFY, A.numel(), cap, 1, kt), workspace, A.device)
+    _check("pss_verify", _lib.pss_verify(A.data_ptr(), A.numel(), kt, cand.data_ptr(), cap,
+                                         n_cand.data_ptr() if n_cand is not None else None,
+                                         out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         _stream(stream)))
+    return out[:cap]
+
+
+def pss_report(cand: torch.Tensor, exact: torch.Tensor, n: int, k: int,
+               n_cand: torch.Tensor | None = None, out=None, stream=None):
+    """The verified k-majority answer: (items, counts uint64, length[1]) on the device."""
+    kt = _key_type(cand)
+    cap = cand.numel()
+    if out is None:
+        out = (torch.empty((max(cap, 1),), dtype=cand.dtype, device=cand.device),
+               torch.empty((max(cap, 1),), dtype=torch.uint64, device=cand.device),
+               torch.zeros((1,), dtype=torch.uint32, device=cand.device))
+    oi, oc, ol = out
+    _check("pss_report", _lib.pss_report(cand.data_ptr(), cap,
+                                         n_cand.data_ptr() if n_cand is not None else None,
+                                         exact.data_ptr(), kt, n, k, oi.data_ptr(), oc.data_ptr(),
+                                         ol.data_ptr(), _stream(stream)))
+    return oi, oc, ol
+
+
+def pss_query(A: torch.Tensor, k: int, P: int, workspace: torch.Tensor | None = None, stream=None):
+    """The k-majority set of A: (items[k], counts[k] uint64, length[1]) device tensors."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    items = torch.empty((k,), dtype=_key_dtype(kt), device=A.device)
+    counts = torch.empty((k,), dtype=torch.uint64, device=A.device)
+    length = torch.zeros((1,), dtype=torch.uint32, device=A.device)
+    ws = _ws(pss_workspace_bytes(OP_QUERY, A.numel(), k, P, kt), workspace, A.device)
+    _check("pss_query", _lib.pss_query(A.data_ptr(), A.numel(), kt, k, P, items.data_ptr(),
+                                       counts.data_ptr(), length.data_ptr(), ws.data_ptr(),
+                                       ws.numel(), _stream(stream)))
+    return items, counts, length
+
+
+def pss_query_host(A_host: torch.Tensor, k: int, P: int, d_A: torch.Tensor | None = None,
+                   workspace: torch.Tensor | None = None, out=None, stream=None, sync=True):
+    """End-to-end query from a HOST tensor (pinned recommended): H2D copy, the whole path, D2H of
+    the result -- all inside the C call. Returns (items, counts) host tensors of the result."""
+    if A_host.is_cuda:
+        raise ValueError("A_host must be a host tensor")
+    kt = _key_type(A_host)
+    n = A_host.numel()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_A = d_A if d_A is not None else torch.empty((max(n, 1),), dtype=A_host.dtype, device=dev)
+    ws = _ws(pss_workspace_bytes(OP_QUERY, n, k, P, kt), workspace, dev)
+    if out is None:
+        pin = torch.cuda.is_available()
+        out = (torch.empty((k,), dtype=_key_dtype(kt), pin_memory=pin),
+               torch.empty((k,), dtype=torch.uint64, pin_memory=pin),
+               torch.zeros((1,), dtype=torch.uint32, pin_memory=pin))
+    oi, oc, ol = out
+    _check("pss_query_host", _lib.pss_query_host(A_host.data_ptr(), d_A.data_ptr(), n, kt, k, P,
+                                                 oi.data_ptr(), oc.data_ptr(), ol.data_ptr(),
+                                                 ws.data_ptr(), ws.numel(), _stream(stream)))
+    if sync:
+        (stream or torch.cuda.current_stream()).synchronize()
+        ln = int(ol[0].item())
+        return oi[:ln], oc[:ln]
+    return out

@@ -1,0 +1,240 @@
+// api.cu -- the C-ABI of libpss.so (include/pss.h): argument validation, workspace layout and
+// launch order. No torch types, no allocation, no global mutable state.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pss {
+
+DevInfo dev_info() {
+  DevInfo d;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return d;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) d.sms = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess)
+    d.smem_optin = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ==
+      cudaSuccess)
+    d.smem_per_sm = v;
+  return d;
+}
+
+static int key_bytes(int kt) { return kt == PSS_KEY_U32 ? 4 : (kt == PSS_KEY_U64 ? 8 : 0); }
+
+static bool summaries_ok(const pss_summaries* s) {
+  return s && key_bytes(s->key_type) && s->items && s->counts && s->errs && s->sizes &&
+         s->k >= 2 && s->count >= 1;
+}
+
+static pss_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA; }
+
+// workspace plan of pss_query: leaves, root, candidates, exact counts, output staging, scratch
+struct QLayout {
+  size_t l_items, l_counts, l_errs, l_sizes, r_items, r_counts, r_errs, r_sizes, cand, ncand,
+      exact, o_items, o_counts, o_len, scratch, total;
+};
+static QLayout q_layout(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  QLayout L;
+  Bump b;
+  L.l_items = b.take<unsigned char>((size_t)P * k * kb);
+  L.l_counts = b.take<uint32_t>((size_t)P * k);
+  L.l_errs = b.take<uint32_t>((size_t)P * k);
+  L.l_sizes = b.take<uint32_t>(P);
+  L.r_items = b.take<unsigned char>((size_t)k * kb);
+  L.r_counts = b.take<uint32_t>(k);
+  L.r_errs = b.take<uint32_t>(k);
+  L.r_sizes = b.take<uint32_t>(1);
+  L.cand = b.take<unsigned char>((size_t)k * kb);
+  L.ncand = b.take<uint32_t>(1);
+  L.exact = b.take<uint64_t>(k);
+  L.o_items = b.take<unsigned char>((size_t)k * kb);
+  L.o_counts = b.take<uint64_t>(k);
+  L.o_len = b.take<uint32_t>(1);
+  const size_t sc = std::max({summarize_ws(n, kb, k, P, d), merge_ws(kb, k, P, d),
+                              verify_ws(kb, k, d)});
+  L.scratch = b.take<unsigned char>(sc);
+  L.total = b.bytes();
+  return L;
+}
+
+}  // namespace pss
+
+using namespace pss;
+
+extern "C" {
+
+const char* pss_status_string(pss_status s) {
+  switch (s) {
+    case PSS_OK: return "PSS_OK";
+    case PSS_ERR_INVALID_ARG: return "PSS_ERR_INVALID_ARG";
+    case PSS_ERR_UNSUPPORTED: return "PSS_ERR_UNSUPPORTED";
+    case PSS_ERR_CAPACITY_MISMATCH: return "PSS_ERR_CAPACITY_MISMATCH";
+    case PSS_ERR_WORKSPACE_TOO_SMALL: return "PSS_ERR_WORKSPACE_TOO_SMALL";
+    case PSS_ERR_CUDA: return "PSS_ERR_CUDA";
+  }
+  return "PSS_UNKNOWN_STATUS";
+}
+
+const char* pss_version(void) { return "pss-b200 0.1 (sm_100a)"; }
+
+size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_type kt) {
+  const int kb = key_bytes(kt);
+  if (!kb) return 0;
+  const DevInfo d = dev_info();
+  switch (op) {
+    case PSS_OP_SUMMARIZE: return summarize_ws(n, kb, k, P, d);
+    case PSS_OP_MERGE: return merge_ws(kb, k, P ? P : 1, d);
+    case PSS_OP_COMBINE: return combine_ws(kb, k, P, d);
+    case PSS_OP_VERIFY: return verify_ws(kb, k, d);
+    case PSS_OP_QUERY: return q_layout(n, kb, k, P ? P : 1, d).total;
+  }
+  return 0;
+}
+
+pss_status pss_summarize(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, uint32_t P,
+                         pss_summaries* leaves, void* d_ws, size_t ws_bytes,
+                         cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || P == 0 || !leaves || (n && !d_A) || !d_ws) return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N || k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (!summaries_ok(leaves)) return PSS_ERR_INVALID_ARG;
+  if (leaves->k != k || leaves->key_type != (int32_t)kt || leaves->count != P)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const DevInfo d = dev_info();
+  if (ws_bytes < summarize_ws(n, kb, k, P, d)) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(summarize_launch(d_A, n, kb, k, P, leaves->items, leaves->counts,
+                                      leaves->errs, leaves->sizes, d_ws, stream, d));
+}
+
+pss_status pss_merge(const pss_summaries* leaves, pss_summaries* root, void* d_ws,
+                     size_t ws_bytes, cudaStream_t stream) {
+  if (!summaries_ok(leaves) || !summaries_ok(root) || !d_ws) return PSS_ERR_INVALID_ARG;
+  if (leaves->k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (root->k != leaves->k || root->key_type != leaves->key_type || root->count != 1)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const int kb = key_bytes(leaves->key_type);
+  const DevInfo d = dev_info();
+  if (ws_bytes < merge_ws(kb, leaves->k, leaves->count, d)) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(merge_tree_launch(kb, leaves->k, leaves->count, leaves->items,
+                                       leaves->counts, leaves->errs, leaves->sizes, root->items,
+                                       root->counts, root->errs, root->sizes, d_ws, stream, d));
+}
+
+pss_status pss_combine(const pss_summaries* a, const pss_summaries* b, pss_summaries* out,
+                       void* d_ws, size_t ws_bytes, cudaStream_t stream) {
+  if (!summaries_ok(a) || !summaries_ok(b) || !summaries_ok(out) || !d_ws)
+    return PSS_ERR_INVALID_ARG;
+  if (a->k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (a->k != b->k || a->k != out->k || a->key_type != b->key_type ||
+      a->key_type != out->key_type || a->count != b->count || a->count != out->count)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const int kb = key_bytes(a->key_type);
+  const DevInfo d = dev_info();
+  if (ws_bytes < combine_ws(kb, a->k, a->count, d)) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(combine_launch(kb, a->k, a->count, a->items, a->counts, a->errs, a->sizes,
+                                    b->items, b->counts, b->errs, b->sizes, out->items,
+                                    out->counts, out->errs, out->sizes, d_ws, stream, d));
+}
+
+pss_status pss_prune(const pss_summaries* root, uint64_t n, void* d_cand, uint32_t* d_n_cand,
+                     cudaStream_t stream) {
+  if (!summaries_ok(root) || !d_cand || !d_n_cand || root->count != 1) return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N) return PSS_ERR_UNSUPPORTED;
+  return cuda_status(prune_launch(key_bytes(root->key_type), root->k, root->items, root->counts,
+                                  root->sizes, n, d_cand, d_n_cand, stream));
+}
+
+pss_status pss_verify(const void* d_A, uint64_t n, pss_key_type kt, const void* d_cand,
+                      uint32_t n_cand, const uint32_t* d_n_cand, uint64_t* d_exact, void* d_ws,
+                      size_t ws_bytes, cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || (n && !d_A) || (n_cand && (!d_cand || !d_exact)) || !d_ws) return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N) return PSS_ERR_UNSUPPORTED;
+  const DevInfo d = dev_info();
+  if (ws_bytes < verify_ws(kb, n_cand, d)) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(verify_launch(d_A, n, kb, d_cand, n_cand, d_n_cand, d_exact, d_ws, stream, d));
+}
+
+pss_status pss_report(const void* d_cand, uint32_t n_cand, const uint32_t* d_n_cand,
+                      const uint64_t* d_exact, pss_key_type kt, uint64_t n, uint32_t k,
+                      void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                      cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || !d_out_len || (n_cand && (!d_cand || !d_exact || !d_out_items || !d_out_counts)))
+    return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N) return PSS_ERR_UNSUPPORTED;
+  return cuda_status(result_launch(kb, n_cand, d_cand, d_n_cand, d_exact, n, k, d_out_items,
+                                   d_out_counts, d_out_len, stream));
+}
+
+static pss_status query_impl(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
+                             void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                             unsigned char* w, const QLayout& L, cudaStream_t s,
+                             const DevInfo& d) {
+  void* li = w + L.l_items;
+  uint32_t* lc = reinterpret_cast<uint32_t*>(w + L.l_counts);
+  uint32_t* le = reinterpret_cast<uint32_t*>(w + L.l_errs);
+  uint32_t* ls = reinterpret_cast<uint32_t*>(w + L.l_sizes);
+  void* ri = w + L.r_items;
+  uint32_t* rc = reinterpret_cast<uint32_t*>(w + L.r_counts);
+  uint32_t* re = reinterpret_cast<uint32_t*>(w + L.r_errs);
+  uint32_t* rs = reinterpret_cast<uint32_t*>(w + L.r_sizes);
+  void* cand = w + L.cand;
+  uint32_t* nc = reinterpret_cast<uint32_t*>(w + L.ncand);
+  uint64_t* exact = reinterpret_cast<uint64_t*>(w + L.exact);
+  void* sc = w + L.scratch;
+  cudaError_t e = summarize_launch(d_A, n, kb, k, P, li, lc, le, ls, sc, s, d);
+  if (e == cudaSuccess) e = merge_tree_launch(kb, k, P, li, lc, le, ls, ri, rc, re, rs, sc, s, d);
+  if (e == cudaSuccess) e = prune_launch(kb, k, ri, rc, rs, n, cand, nc, s);
+  if (e == cudaSuccess) e = verify_launch(d_A, n, kb, cand, k, nc, exact, sc, s, d);
+  if (e == cudaSuccess)
+    e = result_launch(kb, k, cand, nc, exact, n, k, d_out_items, d_out_counts, d_out_len, s);
+  return cuda_status(e);
+}
+
+pss_status pss_query(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, uint32_t P,
+                     void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len, void* d_ws,
+                     size_t ws_bytes, cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || P == 0 || (n && !d_A) || !d_out_items || !d_out_counts || !d_out_len ||
+      !d_ws)
+    return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N || k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  const DevInfo d = dev_info();
+  const QLayout L = q_layout(n, kb, k, P, d);
+  if (ws_bytes < L.total) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return query_impl(d_A, n, kb, k, P, d_out_items, d_out_counts, d_out_len,
+                    static_cast<unsigned char*>(d_ws), L, stream, d);
+}
+
+pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                          uint32_t P, void* h_out_items, uint64_t* h_out_counts,
+                          uint32_t* h_out_len, void* d_ws, size_t ws_bytes,
+                          cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || P == 0 || (n && (!d_A || !h_A)) || !h_out_items || !h_out_counts ||
+      !h_out_len || !d_ws)
+    return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N || k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  const DevInfo d = dev_info();
+  const QLayout L = q_layout(n, kb, k, P, d);
+  if (ws_bytes < L.total) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  unsigned char* w = static_cast<unsigned char*>(d_ws);
+  cudaError_t e = cudaSuccess;
+  if (n) e = cudaMemcpyAsync(d_A, h_A, n * kb, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return PSS_ERR_CUDA;
+  pss_status st = query_impl(d_A, n, kb, k, P, w + L.o_items,
+                             reinterpret_cast<uint64_t*>(w + L.o_counts),
+                             reinterpret_cast<uint32_t*>(w + L.o_len), w, L, stream, d);
+  if (st != PSS_OK) return st;
+  e = cudaMemcpyAsync(h_out_len, w + L.o_len, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h_out_items, w + L.o_items, (size_t)k * kb, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h_out_counts, w + L.o_counts, (size_t)k * 8, cudaMemcpyDeviceToHost,
+                        stream);
+  return cuda_status(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+"""Runner for one pass of the hot path, on one GPU or sharded over several (one process per GPU).
+
+Single GPU: pss_summarize -> pss_merge -> pss_prune -> pss_verify -> pss_report, all C-ABI calls
+on the current stream.
+
+Several GPUs (the paper's hybrid MPI/OpenMP structure):
+rank g owns the contiguous shard [g*n, (g+1)*n) of one stream of world*n keys and the blocks
+[g*P, (g+1)*P) of the global decomposition into world*P blocks. With equal shards those are
+exactly the rank-local blocks (floor(r*n/P) offsets), and with world and P powers of two they
+form one complete subtree of the fixed binary tree (R6). Each rank reduces its subtree to a root;
+ONE all-gather moves the world roots (k counters each) over NVLink, and every rank finishes the
+top log2(world) levels of the same tree in the same order, so the global root is bit-identical to
+the single-GPU one. Verification counts the local shard and ONE all-reduce(sum) adds the exact
+counts. The collectives are torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import (KEY_U32, OP_MERGE, OP_SUMMARIZE, OP_VERIFY, Summaries, _key_dtype, pss_merge,
+               pss_prune, pss_query_host, pss_report, pss_summarize, pss_verify,
+               pss_workspace_bytes)
+
+
+def shard(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """Positions of rank's shard; shards must be equal so block boundaries line up."""
+    if n_total % world:
+        raise ValueError("the stream length must be a multiple of the number of ranks")
+    m = n_total // world
+    return rank * m, (rank + 1) * m
+
+
+def _as_signed(t: torch.Tensor) -> torch.Tensor:
+    """Bit-preserving view with a dtype every backend can move (gloo/NCCL lack uint32)."""
+    m = {torch.uint32: torch.int32, torch.uint64: torch.int64}
+    return t.view(m[t.dtype]) if t.dtype in m else t
+
+
+def gather_summaries(root: Summaries, group=None) -> Summaries:
+    """All-gather one summary per rank into a batch ordered by rank (the next tree level)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = Summaries(torch.empty((world, root.k), dtype=root.items.dtype, device=root.items.device),
+                    torch.empty((world, root.k), dtype=root.counts.dtype, device=root.items.device),
+                    torch.empty((world, root.k), dtype=root.errs.dtype, device=root.items.device),
+                    torch.empty((world,), dtype=root.sizes.dtype, device=root.items.device))
+    for src, dst in ((root.items, out.items), (root.counts, out.counts), (root.errs, out.errs),
+                     (root.sizes, out.sizes)):
+        dist.all_gather_into_tensor(_as_signed(dst).view(-1), _as_signed(src).reshape(-1),
+                                    group=group)
+    return out
+
+
+def allreduce_counts(exact: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+
+    dist.all_reduce(_as_signed(exact), op=dist.ReduceOp.SUM, group=group)
+    return exact
+
+
+class Runner:
+    """Preallocated buffers + one step of the path (see module docstring)."""
+
+    def __init__(self, n: int, k: int, P: int, key_type: int, device, world: int = 1,
+                 rank: int = 0, group=None):
+        if world > 1 and (world & (world - 1) or P & (P - 1)):
+            raise ValueError("sharded runs need power-of-two ranks and blocks per rank")
+        self.n, self.k, self.P, self.kt = n, k, P, key_type
+        self.world, self.rank, self.group = world, rank, group
+        self.dev = torch.device(device)
+        kb = 4 if key_type == KEY_U32 else 8
+        self.leaves = Summaries.empty(P, k, key_type, self.dev)
+        self.root = Summaries.empty(1, k, key_type, self.dev)
+        self.top = Summaries.empty(1, k, key_type, self.dev) if world > 1 else self.root
+        ws = max(pss_workspace_bytes(OP_SUMMARIZE, n, k, P, key_type),
+                 pss_workspace_bytes(OP_MERGE, 0, k, max(P, world), key_type),
+                 pss_workspace_bytes(OP_VERIFY, n, k, 1, key_type))
+        self.ws = torch.empty((ws,), dtype=torch.uint8, device=self.dev)
+        self.exact = torch.zeros((k,), dtype=torch.uint64, device=self.dev)
+        kd = _key_dtype(key_type)
+        self.out = (torch.empty((k,), dtype=kd, device=self.dev),
+                    torch.empty((k,), dtype=torch.uint64, device=self.dev),
+                    torch.zeros((1,), dtype=torch.uint32, device=self.dev))
+        self.host_out = tuple(torch.empty_like(t, device="cpu").pin_memory() for t in self.out)
+        levels = max(1, math.ceil(math.log2(P))) if P > 1 else 1
+        top = max(1, math.ceil(math.log2(world))) if world > 1 else 0
+        # K1 + merge levels (+ top levels) + K3 + K4 (setup, scan, finalize) + K5
+        self.launches_per_step = 1 + levels + top + 1 + 3 + 1
+        self.host_api = "pss_query_host" if world == 1 else "H2D copy + step + D2H (torch)"
+        self._kb = kb
+
+    def step(self, A: torch.Tensor, ev=None):
+        s = torch.cuda.current_stream()
+        if ev is not None:
+            ev[0].record(s)
+        pss_summarize(A, self.k, self.P, out=self.leaves, workspace=self.ws)
+        if ev is not None:
+            ev[1].record(s)
+        pss_merge(self.leaves, out=self.root, workspace=self.ws)
+        n_global = self.n * self.world
+        if self.world > 1:
+            gathered = gather_summaries(self.root, self.group)
+            pss_merge(gathered, out=self.top, workspace=self.ws)
+        if ev is not None:
+            ev[2].record(s)
+        cand, n_cand = pss_prune(self.top, n_global)
+        exact = pss_verify(A, cand, n_cand, out=self.exact, workspace=self.ws)
+        if self.world > 1:
+            allreduce_counts(self.exact, self.group)
+        pss_report(cand, exact, n_global, self.k, n_cand=n_cand, out=self.out)
+        if ev is not None:
+            ev[3].record(s)
+        return self.out
+
+    def result(self):
+        return self.out
+
+    def step_host(self, h_A: torch.Tensor, d_A: torch.Tensor):
+        """End to end from pinned host keys: H2D, the whole path, D2H of the answer."""
+        if self.world == 1:
+            return pss_query_host(h_A, self.k, self.P, d_A=d_A, workspace=None, out=self.host_out,
+                                  sync=False)
+        d_A.copy_(h_A, non_blocking=True)
+        self.step(d_A)
+        for h, d in zip(self.host_out, self.out):
+            h.copy_(d, non_blocking=True)
+        return self.host_out

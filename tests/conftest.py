@@ -26,3 +26,13 @@ LETTERS = {c: i + 1 for i, c in enumerate("abcdefghijklmnopqrstuvwxyz")}
 def letters(s):
     import numpy as np
     return np.array([LETTERS[c] for c in s], dtype=np.uint64)
+
+
+def build_lib():
+    """Build libpss.so without importing the package (its __init__ loads the library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_pss_build", os.path.join(ROOT, "paper_1606_04669_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()

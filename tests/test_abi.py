@@ -1,0 +1,125 @@
+"""CPU-side checks of the boundary: libpss.so loads, exports every symbol include/pss.h declares,
+sizes workspaces, and rejects bad arguments before launching anything (no GPU needed)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pss():
+    from conftest import build_lib
+    build_lib()
+    import paper_1606_04669_b200 as p
+    return p
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "pss.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(pss_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_boundary():
+    fns = header_functions()
+    for f in ["pss_summarize", "pss_merge", "pss_combine", "pss_prune", "pss_verify", "pss_query",
+              "pss_query_host", "pss_workspace_bytes", "pss_status_string", "pss_version"]:
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(pss):
+    lib = ctypes.CDLL(pss.lib_path)
+    for f in header_functions():
+        assert hasattr(lib, f), f
+    assert set(header_functions()) == set(pss.EXPORTED_SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", pss.lib_path], capture_output=True,
+                         text=True).stdout
+    for f in header_functions():
+        assert re.search(rf"\bT {f}$", out, re.M), f
+
+
+def test_sm100a_code_only(pss):
+    out = subprocess.run(["cuobjdump", "--list-elf", pss.lib_path], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_status_strings_and_version(pss):
+    lib = pss._lib
+    assert lib.pss_status_string(0) == b"PSS_OK"
+    assert lib.pss_status_string(4) == b"PSS_ERR_WORKSPACE_TOO_SMALL"
+    assert b"sm_100a" in lib.pss_version()
+
+
+def test_workspace_bytes_monotone(pss):
+    for kt in (pss.KEY_U32, pss.KEY_U64):
+        q1 = pss.pss_workspace_bytes(pss.OP_QUERY, 1 << 20, 100, 64, kt)
+        q2 = pss.pss_workspace_bytes(pss.OP_QUERY, 1 << 20, 1000, 64, kt)
+        q3 = pss.pss_workspace_bytes(pss.OP_QUERY, 1 << 20, 1000, 4096, kt)
+        assert 0 < q1 < q2 < q3
+        assert pss.pss_workspace_bytes(pss.OP_MERGE, 0, 1000, 8192, kt) > 0
+        assert pss.pss_workspace_bytes(pss.OP_VERIFY, 0, 1000, 1, kt) > 0
+    assert pss.pss_workspace_bytes(pss.OP_QUERY, 10, 10, 1, 7) == 0  # bad key type
+
+
+def test_validation_before_launch(pss):
+    """Bad arguments return status codes without touching the device."""
+    lib = pss._lib
+    S = pss._Summ
+    dummy = ctypes.c_void_p(0x1000)
+    leaves = S(0, 10, 4, 0x1000, 0x1000, 0x1000, 0x1000)
+    by = ctypes.byref
+    # k < 2
+    assert lib.pss_summarize(dummy, 100, 0, 1, 4, by(leaves), dummy, 1 << 20, None) == 1
+    # P == 0
+    assert lib.pss_summarize(dummy, 100, 0, 10, 0, by(leaves), dummy, 1 << 20, None) == 1
+    # bad key type
+    assert lib.pss_summarize(dummy, 100, 3, 10, 4, by(leaves), dummy, 1 << 20, None) == 1
+    # n > 2^31
+    assert lib.pss_summarize(dummy, (1 << 31) + 1, 0, 10, 4, by(leaves), dummy, 1 << 20, None) == 2
+    # mismatched capacity / key type / count
+    assert lib.pss_summarize(dummy, 100, 0, 11, 4, by(leaves), dummy, 1 << 20, None) == 3
+    assert lib.pss_summarize(dummy, 100, 1, 10, 4, by(leaves), dummy, 1 << 20, None) == 3
+    assert lib.pss_summarize(dummy, 100, 0, 10, 5, by(leaves), dummy, 1 << 20, None) == 3
+    # null leaves / null A
+    assert lib.pss_summarize(dummy, 100, 0, 10, 4, None, dummy, 1 << 20, None) == 1
+    assert lib.pss_summarize(None, 100, 0, 10, 4, by(leaves), dummy, 1 << 20, None) == 1
+    # merge: root must have count 1 and the same k/type
+    root = S(0, 10, 2, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_merge(by(leaves), by(root), dummy, 1 << 30, None) == 3
+    root = S(1, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_merge(by(leaves), by(root), dummy, 1 << 30, None) == 3
+    # combine: mismatched k
+    b = S(0, 12, 4, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_combine(by(leaves), by(b), by(leaves), dummy, 1 << 30, None) == 3
+    # query: k < 2, P == 0, null outputs
+    assert lib.pss_query(dummy, 100, 0, 1, 4, dummy, dummy, dummy, dummy, 1 << 30, None) == 1
+    assert lib.pss_query(dummy, 100, 0, 10, 0, dummy, dummy, dummy, dummy, 1 << 30, None) == 1
+    assert lib.pss_query(dummy, 100, 0, 10, 4, None, dummy, dummy, dummy, 1 << 30, None) == 1
+    # verify: null candidates with n_cand > 0
+    assert lib.pss_verify(dummy, 100, 0, None, 5, None, dummy, dummy, 1 << 20, None) == 1
+
+
+def test_workspace_too_small_is_reported(pss):
+    lib = pss._lib
+    S = pss._Summ
+    dummy = ctypes.c_void_p(0x1000)
+    leaves = S(0, 1000, 4096, 0x1000, 0x1000, 0x1000, 0x1000)
+    root = S(0, 1000, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_merge(ctypes.byref(leaves), ctypes.byref(root), dummy, 1024, None) == 4
+    assert lib.pss_query(dummy, 1 << 20, 0, 1000, 4096, dummy, dummy, dummy, dummy, 1024, None) == 4
+
+
+def test_product_path_does_not_import_the_oracle():
+    """The product package must not reference oracle/ (parity would be void)."""
+    pkg = os.path.join(ROOT, "paper_1606_04669_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"\boracle\b", src.replace("oracle/", "")), f

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+All arithmetic is integer, so the bar is bit-exact: leaves in slot order, merged summaries and
+the root in canonical order, candidates in root order, exact counts, and the final answer.
+Small cases compare every output; full BASELINE sizes (in bench.py's launch configuration)
+compare sampled leaves one by one plus properties that hold at any size, and the final answer
+against a brute-force histogram.
+"""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pss():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_1606_04669_b200 as p
+    return p
+
+
+def to_dev(A):
+    return torch.from_numpy(np.ascontiguousarray(A)).cuda()
+
+
+def host_summary(S, i=0):
+    return S.host(i)
+
+
+def run_path(pss, A, k, P):
+    dA = to_dev(A)
+    leaves = pss.pss_summarize(dA, k, P)
+    root = pss.pss_merge(leaves)
+    cand, n_cand = pss.pss_prune(root, A.size)
+    exact = pss.pss_verify(dA, cand, n_cand)
+    items, counts, length = pss.pss_query(dA, k, P)
+    torch.cuda.synchronize()
+    nc = int(n_cand.item())
+    ln = int(length.item())
+    return dict(leaves=leaves, root=root,
+                cand=cand[:nc].cpu().numpy().astype(np.uint64).tolist(),
+                exact=exact[:nc].cpu().numpy().astype(np.uint64).tolist(),
+                result=(items[:ln].cpu().numpy().astype(np.uint64).tolist(),
+                        counts[:ln].cpu().numpy().astype(np.uint64).tolist()))
+
+
+def assert_full_parity(pss, A, k, P, threads=8):
+    got = run_path(pss, A, k, P)
+    ref = oracle.pipeline(A, k, P, threads=threads)
+    for r in range(P):
+        assert got["leaves"].host(r) == ref.leaves[r].as_tuples(), f"leaf {r}"
+    assert got["root"].host(0) == ref.root.as_tuples(), "root"
+    assert got["cand"] == ref.cand.tolist()
+    assert got["exact"] == ref.exact.tolist()
+    assert got["result"][0] == ref.result[0].tolist()
+    assert got["result"][1] == ref.result[1].tolist()
+    return got, ref
+
+
+# ---------------------------------------------------------------- small cases, every output
+def test_worked_example_E6(pss, golden):
+    from conftest import letters
+    case = golden["pipeline"][0]
+    A = letters(case["stream"]).astype(np.uint32)
+    got, _ = assert_full_parity(pss, A, case["k"], case["P"])
+    assert got["root"].host(0) == [tuple(x) for x in case["root"]]
+    assert got["result"][0] == case["result"]
+
+
+def test_C1_full(pss):
+    w = inputs.WORKLOADS["C1"]
+    assert_full_parity(pss, w.generate(), w.k, w.P)
+
+
+@pytest.mark.parametrize("n,k,P,s,U", [
+    (1000, 2, 1, 1.1, 50), (1000, 3, 7, 0.8, 20), (4097, 5, 3, 1.3, 1000), (777, 31, 5, 1.1, 100),
+    (5000, 33, 9, 1.1, 400), (12345, 64, 13, 1.05, 5000), (3, 10, 5, 1.1, 10),     # P > n
+    (50, 100, 3, 1.1, 1000),                                                           # k > n
+    (100_000, 8, 3, 1.5, 30), (65_536, 1000, 1, 1.1, 1e6), (200_000, 2, 16, 0.6, 1e5),
+    (131_072, 257, 2, 1.1, 1e8), (0, 10, 4, 1.1, 10), (1, 2, 1, 1.1, 10)])
+def test_random_small(pss, n, k, P, s, U):
+    A = inputs.zipf(n, s, U, seed=n * 7 + k)
+    assert_full_parity(pss, A, k, P)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_tiny_universe_hazards(pss, seed):
+    """Tiny universes and tiny k force fill->evict inside a 32-item window, exhausted minimum
+    levels and victim-hit hazards in almost every window."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 20000))
+    U = int(rng.integers(2, 12))
+    k = int(rng.integers(2, 9))
+    P = int(rng.integers(1, 9))
+    A = rng.integers(0, U, size=n).astype(np.uint32) * np.uint32(2654435761 & 0xFFFFFFFF)
+    assert_full_parity(pss, A.astype(np.uint32), k, P)
+
+
+def test_all_equal_and_all_distinct(pss):
+    assert_full_parity(pss, np.full(70_000, 42, np.uint32), 10, 3)
+    A = np.random.default_rng(1).permutation(np.arange(100_000, dtype=np.uint32)) * 7
+    assert_full_parity(pss, A.astype(np.uint32), 50, 4)
+    assert_full_parity(pss, A.astype(np.uint32), 1000, 2)
+
+
+def test_extreme_keys(pss):
+    """0 and all-ones are ordinary ids (R12): nothing may use a key as a sentinel."""
+    rng = np.random.default_rng(5)
+    A = rng.choice(np.array([0, 0xFFFFFFFF, 0xFFFFFFFE, 1, 7], np.uint32), size=30_000,
+                   p=[0.3, 0.3, 0.2, 0.1, 0.1])
+    assert_full_parity(pss, A, 3, 5)
+    B = rng.choice(np.array([0, 2**64 - 1, 2**64 - 2, 1 << 63, 5], np.uint64), size=30_000)
+    assert_full_parity(pss, B, 2, 3)
+
+
+@pytest.mark.parametrize("n,k,P", [(300_000, 100, 7), (1 << 20, 2000, 16), (100_001, 3, 5)])
+def test_u64_keys_with_tail(pss, n, k, P):
+    A = inputs.zipf(n, 1.8, float(1 << 40), seed=5, key_bytes=8, tail_frac=0.01)
+    assert_full_parity(pss, A, k, P)
+
+
+@pytest.mark.parametrize("k", [5000, 20000])
+def test_large_k_global_state(pss, k):
+    """Summaries too large for shared memory (C4's k >= 5000) take the global-memory path."""
+    A = inputs.zipf(1 << 19, 1.5, float(1 << 32), seed=4)
+    assert_full_parity(pss, A, k, 8)
+
+
+def test_several_tiles_and_ragged_tail(pss):
+    """n = 2^22 + 12345 with 65 536-item-ish blocks, k = 1000, Zipf(1.1): many TMA stages per
+    block, unaligned block starts, and a ragged array end."""
+    A = inputs.zipf((1 << 22) + 12345, 1.1, 1e8, seed=2)
+    assert_full_parity(pss, A, 1000, 64, threads=16)
+
+
+def test_unaligned_device_pointer(pss):
+    A = inputs.zipf(100_003, 1.1, 1e5, seed=11)
+    big = torch.from_numpy(np.concatenate([np.zeros(1, np.uint32), A])).cuda()
+    dA = big[1:]  # 4-byte aligned, not 16-byte aligned
+    k, P = 50, 6
+    leaves = pss.pss_summarize(dA, k, P)
+    root = pss.pss_merge(leaves)
+    cand, n_cand = pss.pss_prune(root, A.size)
+    exact = pss.pss_verify(dA, cand, n_cand)
+    torch.cuda.synchronize()
+    ref = oracle.pipeline(A, k, P)
+    for r in range(P):
+        assert leaves.host(r) == ref.leaves[r].as_tuples()
+    assert root.host(0) == ref.root.as_tuples()
+    nc = int(n_cand.item())
+    assert exact[:nc].cpu().numpy().tolist() == ref.exact.tolist()
+
+
+# ---------------------------------------------------------------- COMBINE and verify directly
+def random_summary(rng, k, full, key_bytes=4, pool=None):
+    size = k if full else int(rng.integers(0, k))
+    pool = pool if pool is not None else rng.integers(0, 1 << 31, size=4 * k + 8)
+    items = rng.choice(pool, size=size, replace=False).astype(np.uint64)
+    counts = rng.integers(1, 50, size=size).astype(np.uint64)
+    errs = np.minimum(counts - 1, rng.integers(0, 10, size=size)).astype(np.uint64)
+    return oracle.Summary(items, counts, errs)
+
+
+@pytest.mark.parametrize("k", [2, 3, 17, 100, 1000])
+def test_combine_direct(pss, k):
+    rng = np.random.default_rng(k)
+    count = 24
+    pool = rng.integers(0, 1 << 31, size=3 * k + 4)  # overlapping item sets
+    pairs = [(random_summary(rng, k, i % 3 != 0, pool=pool), random_summary(rng, k, i % 4 != 0, pool=pool))
+             for i in range(count)]
+    def pack(ss):
+        S = pss.Summaries.empty(count, k, pss.KEY_U32)
+        it = np.zeros((count, k), np.uint32)
+        c = np.zeros((count, k), np.uint32)
+        e = np.zeros((count, k), np.uint32)
+        sz = np.zeros(count, np.uint32)
+        for i, s in enumerate(ss):
+            it[i, :len(s)], c[i, :len(s)], e[i, :len(s)] = s.items, s.counts, s.errs
+            sz[i] = len(s)
+        S.items.copy_(torch.from_numpy(it)); S.counts.copy_(torch.from_numpy(c))
+        S.errs.copy_(torch.from_numpy(e)); S.sizes.copy_(torch.from_numpy(sz))
+        return S
+    a, b = pack([p[0] for p in pairs]), pack([p[1] for p in pairs])
+    out = pss.pss_combine(a, b)
+    torch.cuda.synchronize()
+    for i, (s1, s2) in enumerate(pairs):
+        assert out.host(i) == oracle.combine(s1, s2, k).as_tuples(), i
+
+
+def test_verify_duplicates_absent_and_device_count(pss):
+    A = inputs.zipf(500_000, 1.2, 1e4, seed=3)
+    cand = np.array([inputs.mix32(0), 12345, inputs.mix32(0), inputs.mix32(5), 0, 0xFFFFFFFF],
+                    np.uint32)
+    dA = to_dev(A)
+    ex = pss.pss_verify(dA, to_dev(cand))
+    ex2 = pss.pss_verify(dA, to_dev(cand), torch.tensor([3], dtype=torch.uint32).cuda())
+    torch.cuda.synchronize()
+    want = oracle.verify(A, cand).tolist()
+    assert ex.cpu().numpy().tolist() == want
+    assert ex2[:3].cpu().numpy().tolist() == want[:3]
+    many = np.unique(A)[:3000]  # a candidate list too large for the shared-memory table
+    ex3 = pss.pss_verify(dA, to_dev(many))
+    torch.cuda.synchronize()
+    assert ex3.cpu().numpy().tolist() == oracle.verify(A, many).tolist()
+
+
+def test_query_host_end_to_end(pss):
+    A = inputs.zipf(1 << 20, 1.1, 1e6, seed=9)
+    k, P = 200, 16
+    items, counts = pss.pss_query_host(torch.from_numpy(A).pin_memory(), k, P)
+    ref = oracle.pipeline(A, k, P, threads=8)
+    assert items.numpy().astype(np.uint64).tolist() == ref.result[0].tolist()
+    assert counts.numpy().tolist() == ref.result[1].tolist()
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+def bruteforce_kmajority(A, k):
+    u, c = np.unique(A, return_counts=True)
+    sel = c * k > A.size
+    order = np.lexsort((u[sel], -c[sel].astype(np.int64)))
+    return u[sel][order].astype(np.uint64).tolist(), c[sel][order].astype(np.uint64).tolist()
+
+
+FULL = ["C1", "C2", "H", "C3-s0.5", "C3-s1.0", "C3-s1.5", "C3-s2.0", "C3-s3.0", "C4-k200",
+        "C4-k1000", "C4-k5000", "C4-k20000", "C5"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size(pss, name):
+    """BASELINE.json configs at full size, bench.py's launch configuration (k, P): sampled leaves
+    bit-exact; root guarantees (f <= f_hat <= f + err, err <= n/k, no false negatives, sum <= n)
+    with exact f from the oracle's verification; candidates, exact counts and the answer exact;
+    the answer equals the brute-force k-majority set."""
+    w = inputs.WORKLOADS[name]
+    need = w.n * w.key_bytes * 4
+    try:
+        import psutil
+        if psutil.virtual_memory().available < need + (8 << 30):
+            pytest.skip(f"{name} needs ~{need >> 30} GiB of host memory")
+    except ImportError:
+        pass
+    A = w.generate()
+    n, k, P = A.size, w.k, w.P
+    got = run_path(pss, A, k, P)
+    sample = sorted({0, 1, P // 3, P // 2, P - 2, P - 1} | set(range(7, P, max(1, P // 6))))
+    ref_leaves = oracle.leaves(A, k, P, which=sample, threads=inputs.host_threads())
+    for r, ref in zip(sample, ref_leaves):
+        assert got["leaves"].host(r) == ref.as_tuples(), f"{name} leaf {r}"
+    root = got["root"].host(0)
+    items = np.array([x for x, _, _ in root], dtype=np.uint64)
+    f = oracle.verify(A, items).tolist()
+    assert len(root) <= k and sum(c for _, c, _ in root) <= n
+    keyed = [(-c, x) for x, c, _ in root]
+    assert keyed == sorted(keyed)  # canonical order
+    for (x, c, e), fx in zip(root, f):
+        assert fx <= c <= fx + e and e <= n // k
+    thr = oracle.threshold(n, k)
+    assert got["cand"] == [x for x, c, _ in root if c >= thr]
+    assert got["exact"] == oracle.verify(A, np.array(got["cand"], np.uint64)).tolist()
+    want = bruteforce_kmajority(A, k)
+    assert got["result"] == want
+    assert set(want[0]) <= set(items.tolist())  # recall 1

@@ -72,3 +72,9 @@ def test_workload_registry():
     assert w["H"].n == 1 << 29 and w["H"].k == 1000
     assert w["C5"].key_bytes == 8 and w["C5"].P == 32768
     assert np.array_equal(w["H"].generate(5000), w["C2"].generate(5000))
+
+
+def test_ranges_of_the_stream():
+    a = inputs.zipf(50_000, 1.1, 1e8, seed=2)
+    b = inputs.zipf(20_000, 1.1, 1e8, seed=2, start=30_000, threads=3)
+    assert np.array_equal(a[30_000:], b)
