@@ -5,48 +5,147 @@
 // The warp streams its block of A through a shared-memory ring filled by the TMA engine
 // (cp.async.bulk + mbarrier) and applies Space Saving to 32 consecutive items per step with an
 // exact batched rule:
-//   1. each lane looks its item up in a linear-probing hash index (key -> slot);
+//   1. each lane looks its item up in a two-choice, two-way bucketed cuckoo index
+//      (entry = 16-bit fingerprint | 16-bit slot; a lookup reads both candidate buckets with two
+//      independent 8-byte loads, selects the first fingerprint match without branches and
+//      verifies its key; a rare second fingerprint match takes a slow re-check);
 //   2. __match_any_sync groups equal keys; the first lane of a group is its leader, multiplicity =
 //      popcount of the group restricted to the processed prefix;
 //   3. leaders that miss are ranked in stream order; during the fill phase they take slots
 //      size, size+1, ... (R2); once all k counters are occupied they take the lowest-index slots of
-//      B_m = {slots with count == m, the current minimum} in ascending order (R1). B_m is a bitmap.
+//      B_m = {slots with count == m, the current minimum} in ascending order (R1). B_m is a bitmap
+//      consumed left to right through a cursor; at the start of every step, in parallel with the
+//      lookups, lane j fetches the j-th next victim slot and the index entry of its item;
 //   4. the step processes the longest prefix [0, c) of the 32 items for which this equals the
-//      sequential algorithm: c stops before the first miss that finds B_m empty or the counters
-//      full, and before the first hazard where a victim slot is also hit in the window.
-//   5. hits add their multiplicity; misses evict (count m + mult, err m) and re-index the hash.
+//      sequential algorithm: c stops before the first miss that finds no victim left (B_m empty
+//      or beyond the fetched words) or the counters full, and before the first hazard where a
+//      victim slot is also hit in the window;
+//   5. hits add their multiplicity; misses evict (count m + mult, err m), free the victim's index
+//      entry and write their own entry into a free way of their buckets; a read-back settles lanes
+//      that picked the same entry, and the rare leftovers take a serial cuckoo-kick path.
 // Every step consumes >= 1 item, so the result is bit-identical to sequential Space Saving.
+// When the block length allows, count and error share one 32-bit word (count in the low CB bits).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pss {
 
-constexpr uint32_t SS_RING_BYTES = 8192;  // per-warp TMA ring
+#ifdef PSS_STATS  // debug build only (tools/k1_stats.py): event counters of the batched rule
+__device__ unsigned long long g_ss_stats[16];
+#define SS_STAT(i, v)                                                      \
+  do {                                                                     \
+    const unsigned long long _v = (unsigned long long)(v);                 \
+    if (lane == 0) atomicAdd(&g_ss_stats[i], _v);                          \
+  } while (0)
+}  // namespace pss
+extern "C" int pss_debug_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pss::g_ss_stats, sizeof(pss::g_ss_stats));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(pss::g_ss_stats, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+namespace pss {
+#else
+#define SS_STAT(i, v) \
+  do {                \
+  } while (0)
+#endif
+
+constexpr uint32_t SS_RING_BYTES = 2048;  // per-warp TMA ring
 constexpr uint32_t SS_NSTAGE = 4;
 constexpr uint32_t SS_STAGE_BYTES = SS_RING_BYTES / SS_NSTAGE;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
+constexpr double SS_LOAD = 0.30;                  // index load factor (live keys / entries)
+constexpr int SS_MAX_KICKS = 200;
 
-template <typename HT>
-struct HTag {
-  static constexpr HT EMPTY = (HT)~(HT)0;
-  static constexpr HT TOMB = (HT)(~(HT)0 - 1);
+// index entry traits: ET = uint32_t (16-bit fingerprint | 16-bit slot) or uint64_t (32 | 32).
+// A fingerprint never has all bits set, so an EMPTY entry (all ones) never matches one.
+template <typename ET>
+struct Ent;
+template <>
+struct Ent<uint32_t> {
+  using Pos = uint16_t;
+  static constexpr uint32_t EMPTY = 0xffffffffu;
+  static constexpr uint32_t SLOT = 0xffffu;
+  __device__ static __forceinline__ uint32_t make(uint32_t fp, uint32_t v) {
+    return (fp << 16) | v;
+  }
+  __device__ static __forceinline__ uint32_t fp_of(uint32_t h) { return min(h & 0xffffu, 0xfffeu); }
+  __device__ static __forceinline__ bool fp_eq(uint32_t e, uint32_t fp) { return (e >> 16) == fp; }
+  __device__ static __forceinline__ void load2(const uint32_t* T, uint32_t b, uint32_t& e0,
+                                               uint32_t& e1) {
+    const uint64_t v = reinterpret_cast<const uint64_t*>(T)[b];
+    e0 = (uint32_t)v;
+    e1 = (uint32_t)(v >> 32);
+  }
 };
+template <>
+struct Ent<uint64_t> {
+  using Pos = uint32_t;
+  static constexpr uint64_t EMPTY = ~0ull;
+  static constexpr uint64_t SLOT = 0xffffffffull;
+  __device__ static __forceinline__ uint64_t make(uint32_t fp, uint32_t v) {
+    return ((uint64_t)fp << 32) | v;
+  }
+  __device__ static __forceinline__ uint32_t fp_of(uint32_t h) { return min(h, 0xfffffffeu); }
+  __device__ static __forceinline__ bool fp_eq(uint64_t e, uint32_t fp) {
+    return (uint32_t)(e >> 32) == fp;
+  }
+  __device__ static __forceinline__ void load2(const uint64_t* T, uint32_t b, uint64_t& e0,
+                                               uint64_t& e1) {
+    const ulonglong2 v = reinterpret_cast<const ulonglong2*>(T)[b];
+    e0 = v.x;
+    e1 = v.y;
+  }
+};
+
+__device__ __forceinline__ uint32_t fold32(uint32_t x) { return x; }
+__device__ __forceinline__ uint32_t fold32(uint64_t x) {
+  return (uint32_t)((x * 0x9E3779B97F4A7C15ull) >> 32) ^ (uint32_t)x;
+}
+
+// bucket pair + fingerprint of a key (seeded so that a failed build can rehash). b1 == b2 is
+// allowed: the key then has two candidate entries instead of four.
+template <typename ET, typename KT>
+__device__ __forceinline__ void key_hash(KT x, uint32_t seed, uint32_t NB, uint32_t& b1,
+                                         uint32_t& b2, uint32_t& fp) {
+  const uint32_t ha = (fold32(x) ^ seed) * 0x9E3779B1u;
+  const uint32_t hb = (ha ^ (ha >> 16)) * 0x85EBCA6Bu;
+  b1 = __umulhi(ha, NB);
+  b2 = __umulhi(hb, NB);
+  fp = Ent<ET>::fp_of(hb);
+}
 
 struct SSLayout {
-  size_t keys, cnt, err, bm, vic, ht, total;
-  uint32_t logH;
+  size_t keys, cnt, err, pos, bm, vic, T, total;
+  uint32_t NB;
 };
 
-static SSLayout ss_layout(uint32_t k, int kb, int htb) {
+static double ss_load() {
+  const char* s = std::getenv("PSS_DEBUG_INDEX_LOAD");  // test hook: crowd the index
+  if (s) {
+    double v = std::atof(s);
+    if (v > 0.05 && v <= 0.85) return v;  // 2-way 2-choice cuckoo holds up to ~0.89
+  }
+  return SS_LOAD;
+}
+
+static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed) {
   SSLayout L;
   const size_t KP = align_up(k, 32);
-  L.logH = ceil_log2(4ull * k);  // load factor of live keys <= 1/4
-  L.keys = 0;
-  L.cnt = L.keys + KP * kb;
-  L.err = L.cnt + KP * 4;
-  L.bm = L.err + KP * 4;
-  L.vic = L.bm + KP / 32 * 4;
-  L.ht = L.vic + 32 * 4;
-  L.total = align_up(L.ht + ((size_t)1 << L.logH) * htb, 128);
+  L.NB = (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * ss_load())));
+  Bump b;
+  L.keys = b.take<unsigned char>(KP * kb);
+  L.cnt = b.take<uint32_t>(KP);
+  L.err = packed ? L.cnt : b.take<uint32_t>(KP);
+  L.pos = b.take<unsigned char>(KP * (eb == 4 ? 2 : 4));
+  L.bm = b.take<uint32_t>(KP / 32 + 2);
+  L.vic = b.take<uint32_t>(32);
+  L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
+  L.total = align_up(b.bytes(), 128);
   return L;
 }
 
@@ -61,71 +160,40 @@ struct SumArgs {
   uint32_t* queue;
   unsigned char* gstate;  // per-CTA state when it does not fit shared memory
   size_t gstride;
-  size_t o_cnt, o_err, o_bm, o_vic, o_ht;
-  uint32_t logH;
+  size_t o_cnt, o_err, o_pos, o_bm, o_vic, o_T;
+  uint32_t NB;
+  uint32_t cb;  // PACKED: count in the low cb bits, error above
 };
 
-template <typename KT, typename HT>
-__device__ __forceinline__ int32_t ht_find(const HT* ht, const KT* keys, KT x, uint32_t logH) {
-  const uint32_t mask = (1u << logH) - 1u;
-  uint32_t h = hslot(x, logH);
-  while (true) {
-    const HT e = ht[h];
-    if (e == HTag<HT>::EMPTY) return -1;
-    if (e != HTag<HT>::TOMB && keys[e] == x) return (int32_t)e;
-    h = (h + 1u) & mask;
-  }
-}
-
-// insert slot v for key x (x absent); returns true if an EMPTY entry was consumed
-template <typename KT, typename HT>
-__device__ __forceinline__ bool ht_insert(HT* ht, KT x, uint32_t v, uint32_t logH) {
-  const uint32_t mask = (1u << logH) - 1u;
-  uint32_t h = hslot(x, logH);
-  volatile HT* vh = ht;
-  while (true) {
-    const HT e = vh[h];
-    if (e == HTag<HT>::EMPTY || e == HTag<HT>::TOMB) {
-      const HT old = atomicCAS(&ht[h], e, (HT)v);
-      if (old == e) return e == HTag<HT>::EMPTY;
-      continue;
-    }
-    h = (h + 1u) & mask;
-  }
-}
-
-template <typename KT, typename HT>
-__device__ __forceinline__ void ht_delete(HT* ht, KT y, uint32_t v, uint32_t logH) {
-  const uint32_t mask = (1u << logH) - 1u;
-  uint32_t h = hslot(y, logH);
-  while (ht[h] != (HT)v) h = (h + 1u) & mask;
-  ht[h] = HTag<HT>::TOMB;
-}
-
-template <typename KT, typename HT, bool GSTATE>
+template <typename KT, typename ET, bool GSTATE, bool PACKED>
 __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
+  using EN = Ent<ET>;
+  using PT = typename EN::Pos;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t lane = threadIdx.x;
   const uint32_t ltm = lanemask_lt();
   constexpr uint32_t ST = SS_STAGE_BYTES / sizeof(KT);  // items per stage
-  constexpr uint32_t RING = SS_NSTAGE * ST;
+  constexpr uint32_t RMASK = SS_NSTAGE * ST - 1;
   constexpr uint32_t E = 16 / sizeof(KT);  // items per 16 bytes
 
   KT* ring = reinterpret_cast<KT*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SS_RING_BYTES);
   unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + 64;
   KT* keys = reinterpret_cast<KT*>(st);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);  // count (| err << cb if PACKED)
   uint32_t* err = reinterpret_cast<uint32_t*>(st + a.o_err);
+  PT* pos = reinterpret_cast<PT*>(st + a.o_pos);
   uint32_t* bm = reinterpret_cast<uint32_t*>(st + a.o_bm);
   uint32_t* vic = reinterpret_cast<uint32_t*>(st + a.o_vic);
-  HT* ht = reinterpret_cast<HT*>(st + a.o_ht);
+  ET* T = reinterpret_cast<ET*>(st + a.o_T);
 
   const KT* __restrict__ A = reinterpret_cast<const KT*>(a.A);
   const uint64_t n = a.n;
-  const uint32_t k = a.k, P = a.P, logH = a.logH;
-  const uint32_t H = 1u << logH;
+  const uint32_t k = a.k, P = a.P, NB = a.NB;
+  const uint32_t NE = 2 * NB;
   const uint32_t kw = (k + 31u) / 32u;
+  const uint32_t cb = a.cb;
+  const uint32_t CM = PACKED ? ((1u << cb) - 1u) : 0xffffffffu;
   const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
   const uint64_t nfloor = aligned ? (n & ~(uint64_t)(E - 1)) : 0;
 
@@ -133,6 +201,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     for (uint32_t j = 0; j < SS_NSTAGE; ++j) mbar_init(&bars[j], 1);
     fence_mbar_init();
   }
+  for (uint32_t i = kw + lane; i < kw + 2; i += 32) bm[i] = 0;  // guard words
   __syncwarp();
   uint32_t phasebits = 0;
 
@@ -143,40 +212,99 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     if (r >= P) break;
     const uint64_t lo = (uint64_t)r * n / P;  // Alg. 1 l.3-4: r*n < 2^63 as n <= 2^31
     const uint64_t hi = (uint64_t)(r + 1) * n / P;
+    const uint32_t L = (uint32_t)(hi - lo);
 
     // ---- reset the summary
-    for (uint32_t i = lane; i < H; i += 32) ht[i] = HTag<HT>::EMPTY;
-    uint32_t size = 0, m = 0, bmcount = 0, bmf = 0, nempty = H;
-    bool full = false;
+    for (uint32_t i = lane; i < NE; i += 32) T[i] = EN::EMPTY;
+    uint32_t size = 0, m = 0, bmcount = 0, cur = 0, seed = 0;
     __syncwarp();
 
-    auto new_level = [&]() {  // m = min count, B_m = {slots with count m}
+    auto new_level = [&]() {  // m = min count, B_m = {slots with count m}, cursor at slot 0
       uint32_t mn = 0xffffffffu;
-      for (uint32_t t = lane; t < k; t += 32) mn = min(mn, cnt[t]);
+      for (uint32_t t = lane; t < k; t += 32) mn = min(mn, cnt[t] & CM);
       m = __reduce_min_sync(PSS_FULL, mn);
       uint32_t tot = 0;
       for (uint32_t w = 0; w < kw; ++w) {
         const uint32_t t = w * 32 + lane;
-        const uint32_t bits = __ballot_sync(PSS_FULL, t < k && cnt[t] == m);
+        const uint32_t bits = __ballot_sync(PSS_FULL, t < k && (cnt[t] & CM) == m);
         if (lane == 0) bm[w] = bits;
         tot += __popc(bits);
       }
       bmcount = tot;
-      bmf = 0;
+      cur = 0;
       __syncwarp();
-    };
-    auto ht_rebuild = [&]() {  // drop tombstones
-      for (uint32_t i = lane; i < H; i += 32) ht[i] = HTag<HT>::EMPTY;
-      __syncwarp();
-      for (uint32_t t = lane; t < size; t += 32) ht_insert<KT, HT>(ht, keys[t], t, logH);
-      __syncwarp();
-      nempty = H - size;
     };
 
-    if (lo < hi) {
+    // serial insert of (cx -> slot cv) by the calling lane, cuckoo kicks; false if homeless
+    auto slow_insert = [&](KT cx, uint32_t cv) -> bool {
+      uint32_t prev = 0xffffffffu;
+      for (int step = 0; step < SS_MAX_KICKS; ++step) {
+        uint32_t b1, b2, fp;
+        key_hash<ET>(cx, seed, NB, b1, b2, fp);
+        const uint32_t cand[4] = {2 * b1, 2 * b1 + 1, 2 * b2, 2 * b2 + 1};
+        for (int j = 0; j < 4; ++j) {
+          if (T[cand[j]] == EN::EMPTY) {
+            T[cand[j]] = EN::make(fp, cv);
+            pos[cv] = (PT)cand[j];
+            return true;
+          }
+        }
+        const uint32_t kb = (b1 != prev) ? b1 : b2;
+        const uint32_t idx = 2 * kb + ((step ^ (cv & 1)) & 1);
+        const ET e = T[idx];
+        T[idx] = EN::make(fp, cv);
+        pos[cv] = (PT)idx;
+        cv = (uint32_t)(e & EN::SLOT);
+        cx = keys[cv];
+        prev = kb;
+      }
+      return false;
+    };
+    auto rehash = [&](uint32_t nslots) {  // rebuild the whole index under a new seed (all lanes)
+      bool ok = false;
+      while (!ok) {
+        ++seed;
+        for (uint32_t i = lane; i < NE; i += 32) T[i] = EN::EMPTY;
+        __syncwarp();
+        uint32_t okl = 1;
+        if (lane == 0)
+          for (uint32_t t = 0; t < nslots && okl; ++t) okl = slow_insert(keys[t], t);
+        ok = __shfl_sync(PSS_FULL, okl, 0) != 0;
+        __syncwarp();
+      }
+    };
+    // Fast insert of x -> slot v into the snapshot's first free entry `fi`, then read back;
+    // lanes that lost a race (or had no free entry) insert serially. `nslots` bounds a rehash.
+    auto insert_all = [&](bool ins, KT x, uint32_t v, uint32_t fi, uint32_t fp, uint32_t nslots) {
+      const ET mine = EN::make(fp, v);
+      if (ins && fi != 0xffffffffu) T[fi] = mine;
+      __syncwarp();
+      const bool won = ins && fi != 0xffffffffu && T[fi] == mine;
+      if (won) pos[v] = (PT)fi;
+      uint32_t need = __ballot_sync(PSS_FULL, ins && !won);
+      SS_STAT(2, __popc(need));
+      SS_STAT(10, __popc(__ballot_sync(PSS_FULL, ins && fi == 0xffffffffu)));
+      if (need) {
+        bool failed = false;
+        while (need) {
+          const uint32_t l = __ffs(need) - 1;
+          uint32_t okl = 1;
+          if (lane == l) okl = slow_insert(x, v);
+          failed |= __shfl_sync(PSS_FULL, okl, l) == 0;
+          __syncwarp();
+          need &= need - 1;
+        }
+        if (failed) {
+          SS_STAT(3, 1);
+          rehash(nslots);
+        }
+      }
+    };
+
+    if (L) {
       const uint64_t gbase = aligned ? (lo & ~(uint64_t)(E - 1)) : lo;
-      const uint32_t total = (uint32_t)((hi - gbase + ST - 1) / ST);
-      uint32_t issued = 0, ready = 0;
+      const uint32_t roff = (uint32_t)(lo - gbase);  // ring offset of item lo
+      const uint32_t total = (roff + L + ST - 1) / ST;
       auto issue = [&](uint32_t g) {
         const uint64_t a0 = gbase + (uint64_t)g * ST;
         const uint64_t b0 = min(a0 + ST, hi);
@@ -197,127 +325,201 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         }
         for (uint64_t t = be + lane; t < b0; t += 32) dst[t - a0] = A[t];  // unaligned tail
       };
-      while (issued < total && issued < SS_NSTAGE) issue(issued++);
-
-      uint64_t pos = lo;
-      while (pos < hi) {
-        const uint32_t nv = (uint32_t)min((uint64_t)32, hi - pos);
-        const uint32_t gf = (uint32_t)((pos - gbase) / ST);
-        const uint32_t gl = (uint32_t)((pos + nv - 1 - gbase) / ST);
-        if (issued < total && issued < gf + SS_NSTAGE) {
+      // stages 0..NSTAGE-2 in flight; waiting for stage g frees the slot of stage g-2 (a window
+      // spans at most two stages), which is refilled with stage g+2
+      for (uint32_t g = 0; g < min(total, SS_NSTAGE - 1); ++g) issue(g);
+      uint32_t ready = 0;      // stages waited for
+      uint32_t ready_end = 0;  // items of the partition available in the ring: [0, ready_end)
+      auto ensure = [&](uint32_t end) {  // items [0, end) resident in the ring
+        if (end > ready_end) {
           __syncwarp();
-          do {
-            issue(issued);
-            ++issued;
-          } while (issued < total && issued < gf + SS_NSTAGE);
+          while (end > ready_end) {
+            const uint32_t sl = ready % SS_NSTAGE;
+            mbar_wait(&bars[sl], (phasebits >> sl) & 1u);
+            phasebits ^= 1u << sl;
+            if (ready + 2 >= SS_NSTAGE - 1 && ready + 2 < total) issue(ready + 2);
+            ++ready;
+            ready_end = min(L, ready * ST - roff);
+          }
+          __syncwarp();
         }
-        while (ready <= gl) {
-          const uint32_t sl = ready % SS_NSTAGE;
-          mbar_wait(&bars[sl], (phasebits >> sl) & 1u);
-          phasebits ^= 1u << sl;
-          ++ready;
-        }
-        __syncwarp();
+      };
 
-        // ---- one step over the window [pos, pos + nv)
+      // lookup of x: slot s (-1 if not monitored), its packed count ce, the first free entry fi
+      // of its buckets (insert target) and its fingerprint fp
+      auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp) {
+        uint32_t b1, b2;
+        key_hash<ET>(x, seed, NB, b1, b2, fp);
+        ET e0, e1, e2, e3;
+        EN::load2(T, b1, e0, e1);
+        EN::load2(T, b2, e2, e3);
+        const bool q0 = EN::fp_eq(e0, fp), q1 = EN::fp_eq(e1, fp), q2 = EN::fp_eq(e2, fp),
+                   q3 = EN::fp_eq(e3, fp);
+        ET sel = q3 ? e3 : EN::EMPTY;
+        sel = q2 ? e2 : sel;
+        sel = q1 ? e1 : sel;
+        sel = q0 ? e0 : sel;
+        const uint32_t t0 = sel == EN::EMPTY ? 0u : (uint32_t)(sel & EN::SLOT);
+        const KT kx = keys[t0];
+        ce = cnt[t0];
+        const bool hit = act && sel != EN::EMPTY && kx == x;
+        s = hit ? (int32_t)t0 : -1;
+        // a fingerprint match whose key differs: check the other matches (rare)
+        const bool amb = act && !hit && sel != EN::EMPTY;
+        if (__ballot_sync(PSS_FULL, amb)) {
+          SS_STAT(4, 1);
+          if (amb) {
+            const ET ee[4] = {e0, e1, e2, e3};
+            const bool qq[4] = {q0, q1, q2, q3};
+            for (int j = 0; j < 4 && s < 0; ++j) {
+              const uint32_t t = (uint32_t)(ee[j] & EN::SLOT);
+              if (qq[j] && keys[t] == x) {
+                s = (int32_t)t;
+                ce = cnt[t];
+              }
+            }
+          }
+          __syncwarp();
+        }
+        fi = e3 == EN::EMPTY ? 2 * b2 + 1 : 0xffffffffu;
+        fi = e2 == EN::EMPTY ? 2 * b2 : fi;
+        fi = e1 == EN::EMPTY ? 2 * b1 + 1 : fi;
+        fi = e0 == EN::EMPTY ? 2 * b1 : fi;
+      };
+
+      uint32_t q = 0;  // items consumed
+      // ---- fill phase: free counters are taken in slot order (R2)
+      while (q < L && size < k) {
+        const uint32_t nv = min(32u, L - q);
+        ensure(q + nv);
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = act ? ring[(uint32_t)(pos - gbase + lane) & (RING - 1)] : (KT)0;
-        const int32_t s = act ? ht_find<KT, HT>(ht, keys, x, logH) : -1;
-        __syncwarp();
+        const KT x = ring[(roff + q + lane) & RMASK];
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
+        int32_t s;
+        uint32_t ce, fi, fp;
+        lookup(x, act, s, ce, fi, fp);
+        const bool hit = s >= 0;
         const bool leader = act && (grp & ltm) == 0;
-        const uint32_t missL = __ballot_sync(PSS_FULL, leader && s < 0);
-        const uint32_t cs = (leader && s >= 0) ? cnt[s] : 0u;
+        const uint32_t missL = __ballot_sync(PSS_FULL, leader && !hit);
         uint32_t c = nv;
-
-        if (!full) {
-          // fill phase: free counters are taken in slot order (R2)
-          const uint32_t freec = k - size;
-          if ((uint32_t)__popc(missL) > freec) c = nth_set(missL, freec);
-          const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
-          const bool inpre = leader && lane < c;
-          const uint32_t mult = __popc(grp & pm);
-          if (inpre && s >= 0) cnt[s] = cs + mult;
-          bool took = false;
-          if (inpre && s < 0) {
-            const uint32_t v = size + __popc(missL & ltm);
-            keys[v] = x;
-            cnt[v] = mult;
-            err[v] = 0;
-            took = ht_insert<KT, HT>(ht, x, v, logH);
-          }
-          nempty -= __popc(__ballot_sync(PSS_FULL, took));
-          size += __popc(missL & pm);
-          __syncwarp();
-          if (size == k) {
-            full = true;
-            new_level();
-          }
-        } else {
-          // all k counters occupied: misses evict the lowest slots of B_m (R1)
-          const uint32_t M = __popc(missL);
-          const uint32_t Ms = min(M, bmcount);  // bmcount >= 1 here
-          uint32_t vmax = 0;
-          if (Ms) {
-            uint32_t base = 0, w = bmf;
-            while (base < Ms) {
-              const uint32_t word = bm[w];
-              const uint32_t pc = __popc(word);
-              if (base == 0 && pc == 0) bmf = w + 1;
-              const uint32_t rr = base + __popc(word & ltm);
-              if (((word >> lane) & 1u) && rr < Ms) vic[rr] = w * 32 + lane;
-              base += pc;
-              ++w;
-            }
-            __syncwarp();
-            vmax = vic[Ms - 1];
-          }
-          if (Ms < M) c = nth_set(missL, Ms);  // B_m runs out at this miss
-          // hazard: a victim slot whose item is also hit in the window
-          const bool conf = leader && s >= 0 && Ms && cs == m && (uint32_t)s <= vmax;
-          if (__ballot_sync(PSS_FULL, conf)) {
-            uint32_t cpos = 32;
-            if (conf) {
-              uint32_t rr = 0;
-              while (vic[rr] != (uint32_t)s) ++rr;
-              uint32_t mm = missL;
-              for (uint32_t i = 0; i < rr; ++i) mm &= mm - 1u;
-              const uint32_t pr = (uint32_t)(__ffs(mm) - 1);
-              cpos = max(lane, pr);
-            }
-            c = min(c, __reduce_min_sync(PSS_FULL, cpos));
-          }
-          const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
-          const bool inpre = leader && lane < c;
-          const uint32_t mult = __popc(grp & pm);
-          const bool hitm = inpre && s >= 0 && cs == m;
-          if (inpre && s >= 0) {
-            cnt[s] = cs + mult;
-            if (cs == m) atomicAnd(&bm[(uint32_t)s >> 5], ~(1u << ((uint32_t)s & 31u)));
-          }
-          const bool ev = inpre && s < 0;
-          uint32_t v = 0;
-          if (ev) {
-            v = vic[__popc(missL & ltm)];
-            ht_delete<KT, HT>(ht, keys[v], v, logH);
-          }
-          __syncwarp();
-          bool took = false;
-          if (ev) {
-            keys[v] = x;
-            cnt[v] = m + mult;  // "incremented by one" then further hits in the window
-            err[v] = m;
-            atomicAnd(&bm[v >> 5], ~(1u << (v & 31u)));
-            took = ht_insert<KT, HT>(ht, x, v, logH);
-          }
-          bmcount -= __popc(__ballot_sync(PSS_FULL, hitm)) + __popc(missL & pm);
-          nempty -= __popc(__ballot_sync(PSS_FULL, took));
-          __syncwarp();
-          if (bmcount == 0) new_level();
-          if (nempty < (H >> 1)) ht_rebuild();
+        const uint32_t freec = k - size;
+        if ((uint32_t)__popc(missL) > freec) c = nth_set(missL, freec);
+        const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
+        const bool inpre = leader && lane < c;
+        const uint32_t mult = __popc(grp & pm);
+        if (inpre && hit) cnt[s] = ce + mult;
+        const bool ins = inpre && !hit;
+        const uint32_t v = size + __popc(missL & ltm);
+        if (ins) {
+          keys[v] = x;
+          cnt[v] = mult;
+          if (!PACKED) err[v] = 0;
         }
-        pos += c;
+        const uint32_t grow = __popc(missL & pm);
+        insert_all(ins, x, v, fi, fp, size + grow);
+        size += grow;
+        q += c;
+        SS_STAT(8, 1);
+        SS_STAT(1, c);
+        __syncwarp();
+      }
+      if (size == k) new_level();
+
+      // ---- all k counters occupied: misses evict the lowest slots of B_m (R1)
+      while (q < L) {
+        const uint32_t nv = min(32u, L - q);
+        ensure(q + nv);
+        const bool act = lane < nv;
+        const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
+        const KT x = ring[(roff + q + lane) & RMASK];
+        const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
+
+        // victims for this step (independent of the lookups): lane j holds the j-th next slot
+        // of B_m at or after the cursor (two bitmap words) and the index entry of its item
+        uint32_t w0 = cur >> 5;
+        uint32_t wa = bm[w0] & (0xffffffffu << (cur & 31u));
+        while (wa == 0) wa = bm[++w0];  // bmcount >= 1: some later word has a bit
+        const uint32_t wb = bm[w0 + 1];
+        const uint32_t ca = __popc(wa);
+        const uint32_t navail = min(32u, ca + __popc(wb));
+        const uint32_t ra = __popc(wa & ltm), rb = ca + __popc(wb & ltm);
+        if ((wa >> lane) & 1u) vic[ra] = w0 * 32 + lane;
+        if (((wb >> lane) & 1u) && rb < 32) vic[rb] = w0 * 32 + 32 + lane;
+        __syncwarp();
+        const uint32_t myvic = vic[lane];
+        const uint32_t myop = pos[lane < navail ? myvic : 0];
+
+        int32_t s;
+        uint32_t ce, fi, fp;
+        lookup(x, act, s, ce, fi, fp);
+        const bool hit = s >= 0;
+        const uint32_t cs = ce & CM;
+        const bool leader = act && (grp & ltm) == 0;
+        const uint32_t missL = __ballot_sync(PSS_FULL, leader && !hit);
+        const uint32_t rank = __popc(missL & ltm);
+        const uint32_t M = __popc(missL);
+        const uint32_t Ms = min(M, navail);
+        const uint32_t vmax = __shfl_sync(PSS_FULL, myvic, (Ms ? Ms : 1) - 1);
+        uint32_t c = nv;
+        if (Ms < M) {
+          c = nth_set(missL, Ms);  // no victim left for this miss
+          SS_STAT(5, 1);
+        }
+        // hazard: a victim slot whose item is also hit in the window
+        const bool conf = leader && hit && Ms && cs == m && (uint32_t)s <= vmax;
+        if (__ballot_sync(PSS_FULL, conf)) {
+          uint32_t cpos = 32;
+          if (conf) {
+            uint32_t rr = 0;
+            while (vic[rr] != (uint32_t)s) ++rr;
+            uint32_t mm = missL;
+            for (uint32_t i = 0; i < rr; ++i) mm &= mm - 1u;
+            const uint32_t pr = (uint32_t)(__ffs(mm) - 1);
+            cpos = max(lane, pr);
+          }
+          c = min(c, __reduce_min_sync(PSS_FULL, cpos));
+          SS_STAT(6, 1);
+        }
+        const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
+        const bool inpre = leader && lane < c;
+        const uint32_t mult = __popc(grp & pm);
+        // hits: count += multiplicity; a hit counter leaves B_m
+        const bool hup = inpre && hit;
+        const bool hitm = hup && cs == m;
+        uint32_t* const cptr = cnt + (hit ? (uint32_t)s : 0u);
+        const uint32_t cnew = ce + mult;
+        if (hup) *cptr = cnew;
+        if (hitm) atomicAnd(&bm[(uint32_t)s >> 5], ~(1u << ((uint32_t)s & 31u)));
+        // misses: the victim takes the item, count m + multiplicity ("incremented by one" then
+        // further hits in the window), error m; its old item leaves the index
+        const bool ev = inpre && !hit;
+        const uint32_t v = __shfl_sync(PSS_FULL, myvic, rank & 31u);
+        const uint32_t op = __shfl_sync(PSS_FULL, myop, rank & 31u);
+        const uint32_t vnew = PACKED ? ((m + mult) | (m << cb)) : (m + mult);
+        ET* const tdel = T + op;
+        KT* const kptr = keys + v;
+        uint32_t* const vptr = cnt + v;
+        if (ev) {
+          *tdel = EN::EMPTY;
+          *kptr = x;
+          *vptr = vnew;
+          if (!PACKED) err[v] = m;
+        }
+        insert_all(ev, x, v, fi, fp, size);
+        const uint32_t Mp = __popc(missL & pm);
+        const uint32_t last = __shfl_sync(PSS_FULL, myvic, (Mp ? Mp : 1) - 1);
+        if (Mp) cur = last + 1;
+        bmcount -= __popc(__ballot_sync(PSS_FULL, hitm)) + Mp;
+        q += c;
+        SS_STAT(0, 1);
+        SS_STAT(9, Mp);
+        SS_STAT(1, c);
+        if (bmcount == 0) {
+          SS_STAT(7, 1);
+          new_level();
+        }
+        __syncwarp();
       }
     }
 
@@ -326,9 +528,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     uint32_t* oc = a.counts + (size_t)r * k;
     uint32_t* oe = a.errs + (size_t)r * k;
     for (uint32_t t = lane; t < size; t += 32) {
+      const uint32_t ce = cnt[t];
       oi[t] = keys[t];
-      oc[t] = cnt[t];
-      oe[t] = err[t];
+      oc[t] = ce & CM;
+      oe[t] = PACKED ? ce >> cb : err[t];
     }
     if (lane == 0) a.sizes[r] = size;
     __syncwarp();
@@ -337,33 +540,45 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 
 // ------------------------------------------------------------------------------ host side
 struct SSPlan {
-  bool gstate;
+  bool gstate, packed;
+  uint32_t cb;
   SSLayout L;
   size_t smem;
   int grid;
 };
 
-template <typename KT, typename HT, bool G>
+template <typename KT, typename ET, bool G, bool PK>
 static int ss_blocks_per_sm(size_t smem) {
-  auto kern = ss_summarize_kernel<KT, HT, G>;
+  auto kern = ss_summarize_kernel<KT, ET, G, PK>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
   return nb > 0 ? nb : 1;
 }
 
-static SSPlan ss_plan(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
   SSPlan p;
-  SSLayout Ls = ss_layout(k, kb, 2);
-  p.gstate = Ls.total > SS_SMEM_STATE_MAX || k >= 65000u;
+  // count + error in one word: counts <= Lmax need cb bits, errors <= Lmax / k the rest
+  const uint64_t Lmax = (n + P - 1) / P;
+  p.cb = 1;
+  while (p.cb < 32 && (1ull << p.cb) <= Lmax) ++p.cb;
+  p.packed = p.cb < 32 && (Lmax / k) < (1ull << (32 - p.cb));
+  SSLayout Ls = ss_layout(k, kb, 4, p.packed);
+  p.gstate = Ls.total > SS_SMEM_STATE_MAX || 2ull * Ls.NB >= 0xffffull || k >= 0xffffu;
   if (!p.gstate) {
     p.L = Ls;
     p.smem = SS_RING_BYTES + 64 + Ls.total;
-    int nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false>(p.smem)
-                     : ss_blocks_per_sm<uint64_t, uint16_t, false>(p.smem);
+    int nb;
+    if (p.packed)
+      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint32_t, false, true>(p.smem)
+                   : ss_blocks_per_sm<uint64_t, uint32_t, false, true>(p.smem);
+    else
+      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint32_t, false, false>(p.smem)
+                   : ss_blocks_per_sm<uint64_t, uint32_t, false, false>(p.smem);
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)nb * d.sms);
   } else {
-    p.L = ss_layout(k, kb, 4);
+    p.packed = false;
+    p.L = ss_layout(k, kb, 8, false);
     p.smem = SS_RING_BYTES + 64;
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
   }
@@ -371,8 +586,8 @@ static SSPlan ss_plan(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
   return p;
 }
 
-size_t summarize_ws(uint64_t, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
-  SSPlan p = ss_plan(kb, k, P, d);
+size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  SSPlan p = ss_plan(n, kb, k, P, d);
   Bump b;
   b.take<uint32_t>(1);
   if (p.gstate) b.take<unsigned char>(p.L.total * (size_t)p.grid);
@@ -382,7 +597,7 @@ size_t summarize_ws(uint64_t, int kb, uint32_t k, uint32_t P, const DevInfo& d) 
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
                              void* ws, cudaStream_t s, const DevInfo& d) {
-  SSPlan p = ss_plan(kb, k, P, d);
+  SSPlan p = ss_plan(n, kb, k, P, d);
   Bump b;
   const size_t oq = b.take<uint32_t>(1);
   const size_t og = p.gstate ? b.take<unsigned char>(p.L.total * (size_t)p.grid) : 0;
@@ -400,22 +615,31 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.gstride = p.L.total;
   a.o_cnt = p.L.cnt;
   a.o_err = p.L.err;
+  a.o_pos = p.L.pos;
   a.o_bm = p.L.bm;
   a.o_vic = p.L.vic;
-  a.o_ht = p.L.ht;
-  a.logH = p.L.logH;
+  a.o_T = p.L.T;
+  a.NB = p.L.NB;
+  a.cb = p.cb;
   cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   if (!p.gstate) {
-    if (kb == 4)
-      ss_summarize_kernel<uint32_t, uint16_t, false><<<p.grid, 32, p.smem, s>>>(a);
-    else
-      ss_summarize_kernel<uint64_t, uint16_t, false><<<p.grid, 32, p.smem, s>>>(a);
+    if (p.packed) {
+      if (kb == 4)
+        ss_summarize_kernel<uint32_t, uint32_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+      else
+        ss_summarize_kernel<uint64_t, uint32_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+    } else {
+      if (kb == 4)
+        ss_summarize_kernel<uint32_t, uint32_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+      else
+        ss_summarize_kernel<uint64_t, uint32_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+    }
   } else {
     if (kb == 4)
-      ss_summarize_kernel<uint32_t, uint32_t, true><<<p.grid, 32, p.smem, s>>>(a);
+      ss_summarize_kernel<uint32_t, uint64_t, true, false><<<p.grid, 32, p.smem, s>>>(a);
     else
-      ss_summarize_kernel<uint64_t, uint32_t, true><<<p.grid, 32, p.smem, s>>>(a);
+      ss_summarize_kernel<uint64_t, uint64_t, true, false><<<p.grid, 32, p.smem, s>>>(a);
   }
   return cudaGetLastError();
 }

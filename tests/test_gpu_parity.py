@@ -267,3 +267,14 @@ def test_full_size(pss, name):
     want = bruteforce_kmajority(A, k)
     assert got["result"] == want
     assert set(want[0]) <= set(items.tolist())  # recall 1
+
+
+@pytest.mark.parametrize("load", [0.75, 0.85])
+def test_crowded_index_kick_and_rehash_paths(pss, load, monkeypatch):
+    """Force the summary index to 75-85% occupancy (test hook PSS_DEBUG_INDEX_LOAD) so that
+    inserts collide, take the serial cuckoo-kick path and sometimes rebuild the index."""
+    monkeypatch.setenv("PSS_DEBUG_INDEX_LOAD", str(load))
+    for n, k, P, s, U in [(300_000, 100, 5, 1.1, 1e6), (200_000, 37, 3, 0.8, 5e4),
+                          (100_000, 1000, 2, 1.1, 1e8)]:
+        A = inputs.zipf(n, s, U, seed=n + k)
+        assert_full_parity(pss, A, k, P)
