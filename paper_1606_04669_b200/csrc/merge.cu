@@ -5,13 +5,13 @@
 // One CTA per COMBINE. Both summaries are staged in shared memory; S2's items are indexed by a
 // small hash table so each S1 counter finds its match in O(1) (Find/Remove of Alg. 2 l.5-7);
 // unmatched counters get the other summary's minimum (R4: 0 for an unfull summary); Prune(k)
-// orders the <= 2k counters by (count desc, item asc) with a shared-memory bitonic network and
-// keeps the first k (R5). Outputs are in canonical order.
+// orders the <= 2k counters by (count desc, item asc) and keeps the first k (R5). The ordering is
+// a bitonic network over NT threads x EPT elements held in registers: exchanges between elements
+// of one thread stay in registers, exchanges within a warp use shuffles, and only the strides of
+// 32*EPT elements and more go through shared memory. Outputs are in canonical order.
 #include "common.cuh"
 
 namespace pss {
-
-constexpr int MT = 512;  // threads per merge CTA
 
 struct NodeRef {  // a batch of summaries, structure of arrays
   const void* items;
@@ -34,21 +34,24 @@ struct CombArgs {
   uint32_t nblocks;                     // output nodes
   uint32_t nright;                      // blocks < nright have a right node
   uint32_t canon_single;                // a block without right node: 1 = canonicalize, 0 = copy
+  uint32_t sort_out;                    // 1 = canonical order, 0 = top-k set (internal node)
   unsigned char* gscratch;              // per-CTA scratch when it does not fit shared memory
   size_t gstride;
-  size_t o_ucnt, o_uerr, o_dead, o_ht, o_shi, o_slo, o_sidx;
-  uint32_t logH2, NPmax;
+  size_t o_ucnt, o_uerr, o_dead, o_ht, o_x;
+  uint32_t logH2;
+  uint32_t NP;  // sort width
 };
 
 struct MLayout {
-  size_t ukey, ucnt, uerr, dead, ht, shi, slo, sidx, total;
-  uint32_t logH2, NPmax;
+  size_t ukey, ucnt, uerr, dead, ht, x, total;
+  uint32_t logH2, NP;
 };
 
-static MLayout m_layout(uint32_t k, int kb) {
+// NP = sort width (power of two >= 2k); x = exchange buffer for the shared-memory sort passes
+static MLayout m_layout(uint32_t k, int kb, uint32_t NP) {
   MLayout L;
   const size_t U = 2 * (size_t)k;
-  L.NPmax = 1u << ceil_log2(U);
+  L.NP = NP;
   L.logH2 = ceil_log2(2ull * k);
   Bump b;
   L.ukey = b.take<unsigned char>(U * kb);
@@ -56,40 +59,268 @@ static MLayout m_layout(uint32_t k, int kb) {
   L.uerr = b.take<uint32_t>(U);
   L.dead = b.take<uint8_t>(k);
   L.ht = b.take<uint32_t>((size_t)1 << L.logH2);
-  L.shi = b.take<uint32_t>(L.NPmax);
-  L.slo = b.take<unsigned char>((size_t)L.NPmax * kb);
-  L.sidx = b.take<uint32_t>(L.NPmax);
+  L.x = b.take<unsigned char>((size_t)NP * (8 + kb));
   L.total = b.bytes();
   return L;
 }
 
-__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t* red) {
-  v = __reduce_min_sync(PSS_FULL, v);
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+template <int NT>
+__device__ __forceinline__ uint32_t block_reduce(uint32_t v, uint32_t* red, bool is_min) {
+  v = is_min ? __reduce_min_sync(PSS_FULL, v) : __reduce_add_sync(PSS_FULL, v);
+  constexpr int NW = NT / 32;
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[w] = v;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  uint32_t r = 0xffffffffu;
-  for (int i = 0; i < nw; ++i) r = min(r, red[i]);
+  uint32_t r = is_min ? 0xffffffffu : 0u;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) r = is_min ? min(r, red[i]) : r + red[i];
   __syncthreads();
   return r;
 }
 
-template <typename KT, bool G>
-__global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
+// sort element: (hi = ~count, lo = item) ascending == canonical order; idx = union position
+template <typename KT>
+struct SE {
+  uint32_t hi;
+  KT lo;
+  uint32_t idx;
+};
+template <typename KT>
+__device__ __forceinline__ bool se_less(const SE<KT>& a, const SE<KT>& b) {
+  return a.hi < b.hi || (a.hi == b.hi && (a.lo < b.lo || (a.lo == b.lo && a.idx < b.idx)));
+}
+template <typename KT>
+__device__ __forceinline__ SE<KT> se_shfl_xor(const SE<KT>& e, int m) {
+  SE<KT> r;
+  r.hi = __shfl_xor_sync(PSS_FULL, e.hi, m);
+  r.lo = __shfl_xor_sync(PSS_FULL, e.lo, m);
+  r.idx = __shfl_xor_sync(PSS_FULL, e.idx, m);
+  return r;
+}
+
+// bitonic sort of NT*EPT elements, element i = t*EPT + j held by thread t in v[j]
+template <typename KT, int NT, int EPT>
+__device__ __forceinline__ void bitonic(SE<KT> (&v)[EPT], uint32_t* xhi, KT* xlo, uint32_t* xidx) {
+  constexpr uint32_t NP = NT * EPT;
+  const uint32_t t = threadIdx.x;
+#pragma unroll 1
+  for (uint32_t size = 2; size <= NP; size <<= 1) {
+#pragma unroll 1
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < EPT) {  // partner in the same thread (compile-time register indices)
+#pragma unroll
+        for (int s = 1; s < EPT; s <<= 1) {
+          if ((uint32_t)s == stride) {
+#pragma unroll
+            for (int j = 0; j < EPT; ++j) {
+              const int jp = j ^ s;
+              if (jp > j) {
+                const uint32_t i = t * EPT + j;
+                const bool asc = (i & size) == 0;
+                if (se_less(v[jp], v[j]) == asc) {
+                  const SE<KT> tmp = v[j];
+                  v[j] = v[jp];
+                  v[jp] = tmp;
+                }
+              }
+            }
+          }
+        }
+      } else if (stride < 32u * EPT) {  // partner in the same warp
+        const int lm = (int)(stride / EPT);
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const uint32_t i = t * EPT + j;
+          const SE<KT> o = se_shfl_xor(v[j], lm);
+          const bool asc = (i & size) == 0;
+          const bool lower = (i & stride) == 0;
+          const bool take_min = lower == asc;
+          const bool o_less = se_less(o, v[j]);
+          if (o_less == take_min) v[j] = o;
+        }
+      } else {  // through shared memory
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const uint32_t i = t * EPT + j;
+          xhi[i] = v[j].hi;
+          xlo[i] = v[j].lo;
+          xidx[i] = v[j].idx;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const uint32_t i = t * EPT + j;
+          const uint32_t p = i ^ stride;
+          SE<KT> o;
+          o.hi = xhi[p];
+          o.lo = xlo[p];
+          o.idx = xidx[p];
+          const bool asc = (i & size) == 0;
+          const bool take_min = ((i & stride) == 0) == asc;
+          if (se_less(o, v[j]) == take_min) v[j] = o;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// bitonic sort of NP (power of two) elements held in shared memory (large k)
+template <typename KT, int NT>
+__device__ __forceinline__ void bitonic_smem(uint32_t NP, uint32_t* xhi, KT* xlo, uint32_t* xidx) {
+  for (uint32_t size = 2; size <= NP; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = threadIdx.x; i < NP / 2; i += NT) {
+        const uint32_t p = 2 * i - (i & (stride - 1));
+        const uint32_t q = p + stride;
+        const bool asc = (p & size) == 0;
+        const SE<KT> ep{xhi[p], xlo[p], xidx[p]};
+        const SE<KT> eq{xhi[q], xlo[q], xidx[q]};
+        if (se_less(eq, ep) == asc) {
+          xhi[p] = eq.hi;
+          xlo[p] = eq.lo;
+          xidx[p] = eq.idx;
+          xhi[q] = ep.hi;
+          xlo[q] = ep.lo;
+          xidx[q] = ep.idx;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// One radix-select pass over 8-bit digits: hist[0..256) holds the digit histogram of the
+// elements still in play; finds the digit d at which the running count (from the top digit down
+// when `from_top`, else from digit 0 up) reaches `need`, and the count strictly before d in that
+// order. Result in hist[256] (d) and hist[257] (count before). Warp 0 only.
+__device__ __forceinline__ void radix_pick(uint32_t* hist, uint32_t need, bool from_top) {
+  const uint32_t lane = threadIdx.x & 31u;
+  // lane l owns 8 consecutive digits in the scan order
+  uint32_t h[8];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t dig = from_top ? 255u - (lane * 8 + j) : lane * 8 + j;
+    h[j] = hist[dig];
+    s += h[j];
+  }
+  uint32_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(PSS_FULL, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  const uint32_t excl = incl - s;
+  if (excl < need && need <= incl) {
+    uint32_t run = excl;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (run < need && need <= run + h[j]) {
+        hist[256] = from_top ? 255u - (lane * 8 + j) : lane * 8 + j;
+        hist[257] = run;
+      }
+      run += h[j];
+    }
+  }
+}
+
+// Prune(k) for an internal tree node: the k greatest counters by (count desc, item asc) as a
+// set, in no particular order (COMBINE does not depend on the order of its inputs). Radix select
+// of the threshold count C, then of the threshold item among the counters with count C.
+template <typename KT, int NT>
+__device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT* ukey,
+                                  const uint32_t* ucnt, const uint32_t* uerr, const uint8_t* dead,
+                                  uint32_t* hist, uint32_t* red, KT* oi, uint32_t* oc,
+                                  uint32_t* oe, uint32_t* osize) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t live = 0;
+  for (uint32_t i = tid; i < N; i += NT) live += !(i >= n1 && dead[i - n1]);
+  const uint32_t Lv = block_reduce<NT>(live, red, false);
+  const bool all = Lv <= k;
+  uint32_t need = k;
+  uint32_t C = 0;       // threshold count
+  KT K = (KT)0;         // threshold item among count == C (inclusive)
+  bool all_eq = true;   // take every counter with count == C
+  if (!all) {
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
+      __syncthreads();
+      for (uint32_t i = tid; i < N; i += NT) {
+        if (i >= n1 && dead[i - n1]) continue;
+        const uint32_t c = ucnt[i];
+        if ((c & mask) == C) atomicAdd(&hist[(c >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (tid < 32) radix_pick(hist, need, true);
+      __syncthreads();
+      need -= hist[257];
+      C |= hist[256] << shift;
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    // counters with count == C: `need` of them, the smallest items
+    uint32_t eq = 0;
+    for (uint32_t i = tid; i < N; i += NT)
+      eq += !(i >= n1 && dead[i - n1]) && ucnt[i] == C;
+    eq = block_reduce<NT>(eq, red, false);
+    all_eq = eq == need;
+    if (!all_eq) {
+      KT kmask = 0;
+      for (int shift = 8 * (int)sizeof(KT) - 8; shift >= 0; shift -= 8) {
+        for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < N; i += NT) {
+          if (i >= n1 && dead[i - n1]) continue;
+          const KT x = ukey[i];
+          if (ucnt[i] == C && (x & kmask) == K) atomicAdd(&hist[(uint32_t)(x >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) radix_pick(hist, need, false);
+        __syncthreads();
+        need -= hist[257];
+        K |= (KT)hist[256] << shift;
+        kmask |= (KT)255 << shift;
+        __syncthreads();
+      }
+    }
+  }
+  if (tid == 0) hist[258] = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < N; i += NT) {
+    if (i >= n1 && dead[i - n1]) continue;
+    const uint32_t c = ucnt[i];
+    const bool tk = all || c > C || (c == C && (all_eq || ukey[i] <= K));
+    if (tk) {
+      const uint32_t o = atomicAdd(&hist[258], 1u);
+      oi[o] = ukey[i];
+      oc[o] = c;
+      oe[o] = uerr[i];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *osize = hist[258];
+}
+
+// EPT > 0: the sort keeps EPT elements per thread in registers; EPT == 0: shared-memory sort
+template <typename KT, bool G, int NT, int EPT>
+__global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint32_t red[MT / 32];
+  __shared__ uint32_t red[NT / 32];
+  __shared__ uint32_t hist[260];
+  const uint32_t NP = a.NP;
   const uint32_t k = a.k;
-  const int tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x;
   unsigned char* base = G ? a.gscratch + (size_t)blockIdx.x * a.gstride : smem;
   KT* ukey = reinterpret_cast<KT*>(base);
   uint32_t* ucnt = reinterpret_cast<uint32_t*>(base + a.o_ucnt);
   uint32_t* uerr = reinterpret_cast<uint32_t*>(base + a.o_uerr);
   uint8_t* dead = reinterpret_cast<uint8_t*>(base + a.o_dead);
   uint32_t* ht = reinterpret_cast<uint32_t*>(base + a.o_ht);
-  uint32_t* shi = reinterpret_cast<uint32_t*>(base + a.o_shi);
-  KT* slo = reinterpret_cast<KT*>(base + a.o_slo);
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(base + a.o_sidx);
+  uint32_t* xhi = reinterpret_cast<uint32_t*>(base + a.o_x);
+  uint32_t* xidx = xhi + NP;
+  KT* xlo = reinterpret_cast<KT*>(xidx + NP);
   const uint32_t H2 = 1u << a.logH2, hmask = H2 - 1u;
 
   for (uint32_t blk = blockIdx.x; blk < a.nblocks; blk += gridDim.x) {
@@ -106,7 +337,7 @@ __global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
     uint32_t* oe = a.o.errs + (size_t)blk * k;
 
     if (!has_r && !a.canon_single) {  // odd last node carried up unchanged (R6)
-      for (uint32_t t = tid; t < n1; t += MT) {
+      for (uint32_t t = tid; t < n1; t += NT) {
         oi[t] = i1[t];
         oc[t] = c1[t];
         oe[t] = e1[t];
@@ -120,32 +351,34 @@ __global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
 
     // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4)
     uint32_t mn1 = 0xffffffffu, mn2 = 0xffffffffu;
-    for (uint32_t t = tid; t < n1; t += MT) {
+    for (uint32_t t = tid; t < n1; t += NT) {
       ukey[t] = i1[t];
-      ucnt[t] = c1[t];
+      const uint32_t c = c1[t];
+      ucnt[t] = c;
       uerr[t] = e1[t];
-      mn1 = min(mn1, c1[t]);
+      mn1 = min(mn1, c);
     }
-    for (uint32_t t = tid; t < n2; t += MT) {
+    for (uint32_t t = tid; t < n2; t += NT) {
       ukey[n1 + t] = i2[t];
-      ucnt[n1 + t] = c2[t];
+      const uint32_t c = c2[t];
+      ucnt[n1 + t] = c;
       uerr[n1 + t] = e2[t];
       dead[t] = 0;
-      mn2 = min(mn2, c2[t]);
+      mn2 = min(mn2, c);
     }
-    for (uint32_t h = tid; h < H2; h += MT) ht[h] = 0xffffffffu;
-    const uint32_t m1r = block_min(mn1, red);
-    const uint32_t m2r = block_min(mn2, red);
+    for (uint32_t h = tid; h < H2; h += NT) ht[h] = 0xffffffffu;
+    const uint32_t m1r = block_reduce<NT>(mn1, red, true);
+    const uint32_t m2r = block_reduce<NT>(mn2, red, true);
     const uint32_t m1 = n1 == k ? m1r : 0u;
     const uint32_t m2 = n2 == k ? m2r : 0u;
     // index S2's items (Find of Alg. 2 l.5)
-    for (uint32_t t = tid; t < n2; t += MT) {
+    for (uint32_t t = tid; t < n2; t += NT) {
       uint32_t h = hslot(ukey[n1 + t], a.logH2);
       while (atomicCAS(&ht[h], 0xffffffffu, t) != 0xffffffffu) h = (h + 1u) & hmask;
     }
     __syncthreads();
     // counters of S1: matched -> f1 + f2 and Remove from S2; else f1 + m2 (Alg. 2 l.4-13)
-    for (uint32_t t = tid; t < n1; t += MT) {
+    for (uint32_t t = tid; t < n1; t += NT) {
       const KT x = ukey[t];
       uint32_t h = hslot(x, a.logH2);
       uint32_t j;
@@ -161,7 +394,7 @@ __global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
     }
     __syncthreads();
     // remaining counters of S2: f2 + m1 (Alg. 2 l.14-18)
-    for (uint32_t t = tid; t < n2; t += MT)
+    for (uint32_t t = tid; t < n2; t += NT)
       if (!dead[t]) {
         ucnt[n1 + t] += m1;
         uerr[n1 + t] += m1;
@@ -169,52 +402,57 @@ __global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
     __syncthreads();
     // Prune(k) (Alg. 2 l.19): order by (count desc, item asc), keep the first k (R5)
     const uint32_t N = n1 + n2;
-    const uint32_t NP = N <= 1 ? 1u : 1u << ceil_log2(N);
-    uint32_t live = 0;
-    for (uint32_t t = tid; t < NP; t += MT) {
-      const bool valid = t < N && !(t >= n1 && dead[t - n1]);
-      shi[t] = valid ? ~ucnt[t] : 0xffffffffu;  // valid counts are >= 1, so ~count < all-ones
-      slo[t] = valid ? ukey[t] : (KT)0;
-      sidx[t] = valid ? t : 0xffffffffu;
-      live += valid;
+    if (!a.sort_out) {  // internal tree node: the top-k set
+      select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, oi, oc, oe,
+                                a.o.sizes + blk);
+      continue;
     }
-    live = __reduce_add_sync(PSS_FULL, live);
-    __syncthreads();
-    if ((tid & 31) == 0) red[tid >> 5] = live;
-    __syncthreads();
-    uint32_t L = 0;
-    for (int i = 0; i < MT / 32; ++i) L += red[i];
-    __syncthreads();
-    for (uint32_t size = 2; size <= NP; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-        for (uint32_t i = tid; i < NP / 2; i += MT) {
-          const uint32_t p = 2 * i - (i & (stride - 1));
-          const uint32_t q = p + stride;
-          const bool up = (p & size) == 0;
-          const uint32_t hp = shi[p], hq = shi[q];
-          const KT lp = slo[p], lq = slo[q];
-          const bool gt = hp > hq || (hp == hq && (lp > lq || (lp == lq && sidx[p] > sidx[q])));
-          if (gt == up) {
-            shi[p] = hq;
-            shi[q] = hp;
-            slo[p] = lq;
-            slo[q] = lp;
-            const uint32_t t = sidx[p];
-            sidx[p] = sidx[q];
-            sidx[q] = t;
-          }
-        }
-        __syncthreads();
+    if constexpr (EPT > 0) {
+      SE<KT> v[EPT];
+      uint32_t live = 0;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const uint32_t i = tid * EPT + j;
+        const bool valid = i < N && !(i >= n1 && dead[i - n1]);
+        v[j].hi = valid ? ~ucnt[i] : 0xffffffffu;  // valid counts are >= 1: ~count < all-ones
+        v[j].lo = valid ? ukey[i] : (KT)0;
+        v[j].idx = valid ? i : 0xffffffffu;
+        live += valid;
       }
+      const uint32_t Lv = block_reduce<NT>(live, red, false);
+      bitonic<KT, NT, EPT>(v, xhi, xlo, xidx);
+      const uint32_t outn = min(Lv, k);
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const uint32_t i = tid * EPT + j;
+        if (i < outn) {
+          const uint32_t u = v[j].idx;
+          oi[i] = ukey[u];
+          oc[i] = ucnt[u];
+          oe[i] = uerr[u];
+        }
+      }
+      if (tid == 0) a.o.sizes[blk] = outn;
+    } else {
+      uint32_t live = 0;
+      for (uint32_t i = tid; i < NP; i += NT) {
+        const bool valid = i < N && !(i >= n1 && dead[i - n1]);
+        xhi[i] = valid ? ~ucnt[i] : 0xffffffffu;
+        xlo[i] = valid ? ukey[i] : (KT)0;
+        xidx[i] = valid ? i : 0xffffffffu;
+        live += valid;
+      }
+      const uint32_t Lv = block_reduce<NT>(live, red, false);
+      bitonic_smem<KT, NT>(NP, xhi, xlo, xidx);
+      const uint32_t outn = min(Lv, k);
+      for (uint32_t i = tid; i < outn; i += NT) {
+        const uint32_t u = xidx[i];
+        oi[i] = ukey[u];
+        oc[i] = ucnt[u];
+        oe[i] = uerr[u];
+      }
+      if (tid == 0) a.o.sizes[blk] = outn;
     }
-    const uint32_t outn = min(L, k);
-    for (uint32_t t = tid; t < outn; t += MT) {
-      const uint32_t j = sidx[t];
-      oi[t] = ukey[j];
-      oc[t] = ucnt[j];
-      oe[t] = uerr[j];
-    }
-    if (tid == 0) a.o.sizes[blk] = outn;
     __syncthreads();
   }
 }
@@ -222,6 +460,7 @@ __global__ void __launch_bounds__(MT) combine_kernel(const CombArgs a) {
 // ------------------------------------------------------------------------------ host side
 struct MPlan {
   bool g;
+  int nt, ept;
   MLayout L;
   size_t smem;
   int grid_cap;
@@ -229,11 +468,39 @@ struct MPlan {
 
 static MPlan m_plan(int kb, uint32_t k, const DevInfo& d) {
   MPlan p;
-  p.L = m_layout(k, kb);
-  p.g = p.L.total > (size_t)d.smem_optin - 1024;
+  uint32_t NP = 1u << ceil_log2(2ull * k);
+  if (NP < 256) NP = 256;
+  p.nt = (int)std::min<uint32_t>(1024, NP / 2);
+  p.ept = (int)(NP / p.nt);
+  p.L = m_layout(k, kb, NP);
+  p.g = p.L.total > (size_t)d.smem_optin - 2048;
   p.smem = p.g ? 0 : p.L.total;
   p.grid_cap = p.g ? 2 * d.sms : 1 << 30;
   return p;
+}
+
+template <typename KT, bool G, int NT, int EPT>
+static void launch_comb(const CombArgs& a, int grid, size_t smem, cudaStream_t s) {
+  auto kern = combine_kernel<KT, G, NT, EPT>;
+  if (!G) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, NT, G ? 0 : smem, s>>>(a);
+}
+
+template <typename KT, bool G>
+static bool dispatch_comb(const CombArgs& a, int grid, const MPlan& p, cudaStream_t s) {
+  switch (p.nt * 100 + p.ept) {
+    case 128 * 100 + 2: launch_comb<KT, G, 128, 2>(a, grid, p.smem, s); return true;
+    case 256 * 100 + 2: launch_comb<KT, G, 256, 2>(a, grid, p.smem, s); return true;
+    case 512 * 100 + 2: launch_comb<KT, G, 512, 2>(a, grid, p.smem, s); return true;
+    case 1024 * 100 + 2: launch_comb<KT, G, 1024, 2>(a, grid, p.smem, s); return true;
+    case 1024 * 100 + 4: launch_comb<KT, G, 1024, 4>(a, grid, p.smem, s); return true;
+    case 1024 * 100 + 8: launch_comb<KT, G, 1024, 8>(a, grid, p.smem, s); return true;
+  }
+  if (p.nt == 1024 && p.ept > 8) {
+    launch_comb<KT, G, 1024, 0>(a, grid, p.smem, s);
+    return true;
+  }
+  return false;
 }
 
 static cudaError_t combine_run(int kb, uint32_t k, CombArgs a, void* ws, cudaStream_t s,
@@ -246,30 +513,17 @@ static cudaError_t combine_run(int kb, uint32_t k, CombArgs a, void* ws, cudaStr
   a.o_uerr = p.L.uerr;
   a.o_dead = p.L.dead;
   a.o_ht = p.L.ht;
-  a.o_shi = p.L.shi;
-  a.o_slo = p.L.slo;
-  a.o_sidx = p.L.sidx;
+  a.o_x = p.L.x;
   a.logH2 = p.L.logH2;
-  a.NPmax = p.L.NPmax;
+  a.NP = p.L.NP;
   if (a.nblocks == 0) return cudaSuccess;
   const int grid = (int)std::min<uint32_t>(a.nblocks, (uint32_t)p.grid_cap);
-  if (kb == 4) {
-    if (p.g) {
-      combine_kernel<uint32_t, true><<<grid, MT, 0, s>>>(a);
-    } else {
-      cudaFuncSetAttribute(combine_kernel<uint32_t, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      combine_kernel<uint32_t, false><<<grid, MT, p.smem, s>>>(a);
-    }
-  } else {
-    if (p.g) {
-      combine_kernel<uint64_t, true><<<grid, MT, 0, s>>>(a);
-    } else {
-      cudaFuncSetAttribute(combine_kernel<uint64_t, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      combine_kernel<uint64_t, false><<<grid, MT, p.smem, s>>>(a);
-    }
-  }
+  bool ok;
+  if (kb == 4)
+    ok = p.g ? dispatch_comb<uint32_t, true>(a, grid, p, s) : dispatch_comb<uint32_t, false>(a, grid, p, s);
+  else
+    ok = p.g ? dispatch_comb<uint64_t, true>(a, grid, p, s) : dispatch_comb<uint64_t, false>(a, grid, p, s);
+  if (!ok) return cudaErrorInvalidConfiguration;
   return cudaGetLastError();
 }
 
@@ -299,6 +553,7 @@ cudaError_t combine_launch(int kb, uint32_t k, uint32_t count, const void* a_ite
   a.nblocks = count;
   a.nright = count;
   a.canon_single = 1;
+  a.sort_out = 1;
   return combine_run(kb, k, a, ws, s, d);
 }
 
@@ -348,6 +603,7 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
     a.nblocks = 1;
     a.nright = 0;
     a.canon_single = 1;
+    a.sort_out = 1;
     return combine_run(kb, k, a, scratch, s, d);
   }
   uint32_t c = P;
@@ -366,6 +622,7 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
     a.nblocks = cout;
     a.nright = c / 2;
     a.canon_single = 0;
+    a.sort_out = cout == 1;  // internal nodes are top-k sets; the root is canonical (R5)
     cudaError_t e = combine_run(kb, k, a, scratch, s, d);
     if (e != cudaSuccess) return e;
     cur = NodeRef{out.items, out.counts, out.errs, out.sizes};

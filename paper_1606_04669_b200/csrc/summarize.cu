@@ -6,9 +6,9 @@
 // (cp.async.bulk + mbarrier) and applies Space Saving to 32 consecutive items per step with an
 // exact batched rule:
 //   1. each lane looks its item up in a two-choice, two-way bucketed cuckoo index
-//      (entry = 16-bit fingerprint | 16-bit slot; a lookup reads both candidate buckets with two
-//      independent 8-byte loads, selects the first fingerprint match without branches and
-//      verifies its key; a rare second fingerprint match takes a slow re-check);
+//      (entry = fingerprint | slot in 16 bits for k <= 4094; a lookup reads both candidate
+//      buckets with two independent loads, selects the first fingerprint match without branches
+//      and verifies its key; a fingerprint match with another key takes a slow re-check);
 //   2. __match_any_sync groups equal keys; the first lane of a group is its leader, multiplicity =
 //      popcount of the group restricted to the processed prefix;
 //   3. leaders that miss are ranked in stream order; during the fill phase they take slots
@@ -24,8 +24,9 @@
 //      entry and write their own entry into a free way of their buckets; a read-back settles lanes
 //      that picked the same entry, and the rare leftovers take a serial cuckoo-kick path.
 // Every step consumes >= 1 item, so the result is bit-identical to sequential Space Saving.
-// When the block length allows, count and error share one 32-bit word (count in the low CB bits).
+// When the block length allows, count and error share one 32-bit word (count in the low cb bits).
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -58,49 +59,43 @@ constexpr uint32_t SS_RING_BYTES = 2048;  // per-warp TMA ring
 constexpr uint32_t SS_NSTAGE = 4;
 constexpr uint32_t SS_STAGE_BYTES = SS_RING_BYTES / SS_NSTAGE;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
+constexpr uint32_t SS_K_SMALL = 4094;             // 16-bit index entries up to this k
 constexpr double SS_LOAD = 0.30;                  // index load factor (live keys / entries)
 constexpr int SS_MAX_KICKS = 200;
 
-// index entry traits: ET = uint32_t (16-bit fingerprint | 16-bit slot) or uint64_t (32 | 32).
-// A fingerprint never has all bits set, so an EMPTY entry (all ones) never matches one.
+// Index entry layout (runtime): slot in the low sb bits, fingerprint above. A slot field of all
+// ones is never a slot (sb is chosen so that k - 1 < 2^sb - 1) and a fingerprint is never all ones,
+// so the EMPTY entry (all ones) matches no fingerprint.
 template <typename ET>
-struct Ent;
-template <>
-struct Ent<uint32_t> {
-  using Pos = uint16_t;
-  static constexpr uint32_t EMPTY = 0xffffffffu;
-  static constexpr uint32_t SLOT = 0xffffu;
-  __device__ static __forceinline__ uint32_t make(uint32_t fp, uint32_t v) {
-    return (fp << 16) | v;
+struct Ent {
+  static constexpr ET EMPTY = (ET)~(ET)0;
+  uint32_t sb;     // slot bits
+  uint32_t fmask;  // fingerprint field mask (after >> sb)
+  __device__ __forceinline__ ET make(uint32_t fp, uint32_t v) const {
+    return (ET)(((ET)fp << sb) | (ET)v);
   }
-  __device__ static __forceinline__ uint32_t fp_of(uint32_t h) { return min(h & 0xffffu, 0xfffeu); }
-  __device__ static __forceinline__ bool fp_eq(uint32_t e, uint32_t fp) { return (e >> 16) == fp; }
-  __device__ static __forceinline__ void load2(const uint32_t* T, uint32_t b, uint32_t& e0,
-                                               uint32_t& e1) {
-    const uint64_t v = reinterpret_cast<const uint64_t*>(T)[b];
-    e0 = (uint32_t)v;
-    e1 = (uint32_t)(v >> 32);
+  __device__ __forceinline__ uint32_t slot(ET e) const {
+    return (uint32_t)(e & (ET)(((ET)1 << sb) - 1));
   }
+  __device__ __forceinline__ bool fp_eq(ET e, uint32_t fp) const {
+    return (uint32_t)(e >> sb) == fp;
+  }
+  __device__ __forceinline__ uint32_t fp_of(uint32_t h) const { return min(h & fmask, fmask - 1); }
 };
-template <>
-struct Ent<uint64_t> {
-  using Pos = uint32_t;
-  static constexpr uint64_t EMPTY = ~0ull;
-  static constexpr uint64_t SLOT = 0xffffffffull;
-  __device__ static __forceinline__ uint64_t make(uint32_t fp, uint32_t v) {
-    return ((uint64_t)fp << 32) | v;
-  }
-  __device__ static __forceinline__ uint32_t fp_of(uint32_t h) { return min(h, 0xfffffffeu); }
-  __device__ static __forceinline__ bool fp_eq(uint64_t e, uint32_t fp) {
-    return (uint32_t)(e >> 32) == fp;
-  }
-  __device__ static __forceinline__ void load2(const uint64_t* T, uint32_t b, uint64_t& e0,
-                                               uint64_t& e1) {
-    const ulonglong2 v = reinterpret_cast<const ulonglong2*>(T)[b];
-    e0 = v.x;
-    e1 = v.y;
-  }
-};
+
+// both entries of bucket b
+__device__ __forceinline__ void load_bucket(const uint16_t* T, uint32_t b, uint16_t& e0,
+                                            uint16_t& e1) {
+  const uint32_t v = reinterpret_cast<const uint32_t*>(T)[b];
+  e0 = (uint16_t)v;
+  e1 = (uint16_t)(v >> 16);
+}
+__device__ __forceinline__ void load_bucket(const uint64_t* T, uint32_t b, uint64_t& e0,
+                                            uint64_t& e1) {
+  const ulonglong2 v = reinterpret_cast<const ulonglong2*>(T)[b];
+  e0 = v.x;
+  e1 = v.y;
+}
 
 __device__ __forceinline__ uint32_t fold32(uint32_t x) { return x; }
 __device__ __forceinline__ uint32_t fold32(uint64_t x) {
@@ -110,13 +105,13 @@ __device__ __forceinline__ uint32_t fold32(uint64_t x) {
 // bucket pair + fingerprint of a key (seeded so that a failed build can rehash). b1 == b2 is
 // allowed: the key then has two candidate entries instead of four.
 template <typename ET, typename KT>
-__device__ __forceinline__ void key_hash(KT x, uint32_t seed, uint32_t NB, uint32_t& b1,
-                                         uint32_t& b2, uint32_t& fp) {
+__device__ __forceinline__ void key_hash(const Ent<ET>& en, KT x, uint32_t seed, uint32_t NB,
+                                         uint32_t& b1, uint32_t& b2, uint32_t& fp) {
   const uint32_t ha = (fold32(x) ^ seed) * 0x9E3779B1u;
   const uint32_t hb = (ha ^ (ha >> 16)) * 0x85EBCA6Bu;
   b1 = __umulhi(ha, NB);
   b2 = __umulhi(hb, NB);
-  fp = Ent<ET>::fp_of(hb);
+  fp = en.fp_of(hb);
 }
 
 struct SSLayout {
@@ -141,7 +136,7 @@ static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed) {
   L.keys = b.take<unsigned char>(KP * kb);
   L.cnt = b.take<uint32_t>(KP);
   L.err = packed ? L.cnt : b.take<uint32_t>(KP);
-  L.pos = b.take<unsigned char>(KP * (eb == 4 ? 2 : 4));
+  L.pos = b.take<unsigned char>(KP * (eb == 2 ? 2 : 4));
   L.bm = b.take<uint32_t>(KP / 32 + 2);
   L.vic = b.take<uint32_t>(32);
   L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
@@ -162,19 +157,21 @@ struct SumArgs {
   size_t gstride;
   size_t o_cnt, o_err, o_pos, o_bm, o_vic, o_T;
   uint32_t NB;
-  uint32_t cb;  // PACKED: count in the low cb bits, error above
+  uint32_t cb;            // PACKED: count in the low cb bits, error above
+  uint32_t sb, fmask;     // index entry layout
 };
 
 template <typename KT, typename ET, bool GSTATE, bool PACKED>
 __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
-  using EN = Ent<ET>;
-  using PT = typename EN::Pos;
+  using PT = typename std::conditional<sizeof(ET) == 2, uint16_t, uint32_t>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t lane = threadIdx.x;
   const uint32_t ltm = lanemask_lt();
   constexpr uint32_t ST = SS_STAGE_BYTES / sizeof(KT);  // items per stage
   constexpr uint32_t RMASK = SS_NSTAGE * ST - 1;
   constexpr uint32_t E = 16 / sizeof(KT);  // items per 16 bytes
+  constexpr ET EMPTY = Ent<ET>::EMPTY;
+  const Ent<ET> en{a.sb, a.fmask};
 
   KT* ring = reinterpret_cast<KT*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SS_RING_BYTES);
@@ -215,7 +212,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     const uint32_t L = (uint32_t)(hi - lo);
 
     // ---- reset the summary
-    for (uint32_t i = lane; i < NE; i += 32) T[i] = EN::EMPTY;
+    for (uint32_t i = lane; i < NE; i += 32) T[i] = EMPTY;
     uint32_t size = 0, m = 0, bmcount = 0, cur = 0, seed = 0;
     __syncwarp();
 
@@ -240,11 +237,11 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       uint32_t prev = 0xffffffffu;
       for (int step = 0; step < SS_MAX_KICKS; ++step) {
         uint32_t b1, b2, fp;
-        key_hash<ET>(cx, seed, NB, b1, b2, fp);
+        key_hash<ET>(en, cx, seed, NB, b1, b2, fp);
         const uint32_t cand[4] = {2 * b1, 2 * b1 + 1, 2 * b2, 2 * b2 + 1};
         for (int j = 0; j < 4; ++j) {
-          if (T[cand[j]] == EN::EMPTY) {
-            T[cand[j]] = EN::make(fp, cv);
+          if (T[cand[j]] == EMPTY) {
+            T[cand[j]] = en.make(fp, cv);
             pos[cv] = (PT)cand[j];
             return true;
           }
@@ -252,9 +249,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t kb = (b1 != prev) ? b1 : b2;
         const uint32_t idx = 2 * kb + ((step ^ (cv & 1)) & 1);
         const ET e = T[idx];
-        T[idx] = EN::make(fp, cv);
+        T[idx] = en.make(fp, cv);
         pos[cv] = (PT)idx;
-        cv = (uint32_t)(e & EN::SLOT);
+        cv = en.slot(e);
         cx = keys[cv];
         prev = kb;
       }
@@ -264,7 +261,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       bool ok = false;
       while (!ok) {
         ++seed;
-        for (uint32_t i = lane; i < NE; i += 32) T[i] = EN::EMPTY;
+        for (uint32_t i = lane; i < NE; i += 32) T[i] = EMPTY;
         __syncwarp();
         uint32_t okl = 1;
         if (lane == 0)
@@ -276,11 +273,14 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     // Fast insert of x -> slot v into the snapshot's first free entry `fi`, then read back;
     // lanes that lost a race (or had no free entry) insert serially. `nslots` bounds a rehash.
     auto insert_all = [&](bool ins, KT x, uint32_t v, uint32_t fi, uint32_t fp, uint32_t nslots) {
-      const ET mine = EN::make(fp, v);
-      if (ins && fi != 0xffffffffu) T[fi] = mine;
+      const ET mine = en.make(fp, v);
+      const bool tryfi = ins && fi != 0xffffffffu;
+      ET* const tp = T + (tryfi ? fi : 0u);
+      if (tryfi) *tp = mine;
       __syncwarp();
-      const bool won = ins && fi != 0xffffffffu && T[fi] == mine;
-      if (won) pos[v] = (PT)fi;
+      const bool won = tryfi && *tp == mine;
+      PT* const pp = pos + v;
+      if (won) *pp = (PT)fi;
       uint32_t need = __ballot_sync(PSS_FULL, ins && !won);
       SS_STAT(2, __popc(need));
       SS_STAT(10, __popc(__ballot_sync(PSS_FULL, ins && fi == 0xffffffffu)));
@@ -349,42 +349,51 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       // of its buckets (insert target) and its fingerprint fp
       auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp) {
         uint32_t b1, b2;
-        key_hash<ET>(x, seed, NB, b1, b2, fp);
+        key_hash<ET>(en, x, seed, NB, b1, b2, fp);
         ET e0, e1, e2, e3;
-        EN::load2(T, b1, e0, e1);
-        EN::load2(T, b2, e2, e3);
-        const bool q0 = EN::fp_eq(e0, fp), q1 = EN::fp_eq(e1, fp), q2 = EN::fp_eq(e2, fp),
-                   q3 = EN::fp_eq(e3, fp);
-        ET sel = q3 ? e3 : EN::EMPTY;
+        load_bucket(T, b1, e0, e1);
+        load_bucket(T, b2, e2, e3);
+        bool q0 = en.fp_eq(e0, fp), q1 = en.fp_eq(e1, fp), q2 = en.fp_eq(e2, fp),
+             q3 = en.fp_eq(e3, fp);
+        ET sel = q3 ? e3 : EMPTY;
         sel = q2 ? e2 : sel;
         sel = q1 ? e1 : sel;
         sel = q0 ? e0 : sel;
-        const uint32_t t0 = sel == EN::EMPTY ? 0u : (uint32_t)(sel & EN::SLOT);
+        const uint32_t t0 = sel == EMPTY ? 0u : en.slot(sel);
         const KT kx = keys[t0];
         ce = cnt[t0];
-        const bool hit = act && sel != EN::EMPTY && kx == x;
+        const bool hit = act && sel != EMPTY && kx == x;
         s = hit ? (int32_t)t0 : -1;
-        // a fingerprint match whose key differs: check the other matches (rare)
-        const bool amb = act && !hit && sel != EN::EMPTY;
-        if (__ballot_sync(PSS_FULL, amb)) {
+        // a fingerprint match whose key differs: check the other matches in order
+        bool amb = act && !hit && sel != EMPTY;
+        while (__ballot_sync(PSS_FULL, amb)) {
           SS_STAT(4, 1);
           if (amb) {
-            const ET ee[4] = {e0, e1, e2, e3};
-            const bool qq[4] = {q0, q1, q2, q3};
-            for (int j = 0; j < 4 && s < 0; ++j) {
-              const uint32_t t = (uint32_t)(ee[j] & EN::SLOT);
-              if (qq[j] && keys[t] == x) {
+            // drop the first remaining match and take the next one
+            if (q0) q0 = false;
+            else if (q1) q1 = false;
+            else if (q2) q2 = false;
+            else q3 = false;
+            ET nx = q3 ? e3 : EMPTY;
+            nx = q2 ? e2 : nx;
+            nx = q1 ? e1 : nx;
+            nx = q0 ? e0 : nx;
+            if (nx == EMPTY) {
+              amb = false;
+            } else {
+              const uint32_t t = en.slot(nx);
+              if (keys[t] == x) {
                 s = (int32_t)t;
                 ce = cnt[t];
+                amb = false;
               }
             }
           }
-          __syncwarp();
         }
-        fi = e3 == EN::EMPTY ? 2 * b2 + 1 : 0xffffffffu;
-        fi = e2 == EN::EMPTY ? 2 * b2 : fi;
-        fi = e1 == EN::EMPTY ? 2 * b1 + 1 : fi;
-        fi = e0 == EN::EMPTY ? 2 * b1 : fi;
+        fi = e3 == EMPTY ? 2 * b2 + 1 : 0xffffffffu;
+        fi = e2 == EMPTY ? 2 * b2 : fi;
+        fi = e1 == EMPTY ? 2 * b1 + 1 : fi;
+        fi = e0 == EMPTY ? 2 * b1 : fi;
       };
 
       uint32_t q = 0;  // items consumed
@@ -501,7 +510,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         KT* const kptr = keys + v;
         uint32_t* const vptr = cnt + v;
         if (ev) {
-          *tdel = EN::EMPTY;
+          *tdel = EMPTY;
           *kptr = x;
           *vptr = vnew;
           if (!PACKED) err[v] = m;
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 // ------------------------------------------------------------------------------ host side
 struct SSPlan {
   bool gstate, packed;
-  uint32_t cb;
+  uint32_t cb, sb, fmask;
   SSLayout L;
   size_t smem;
   int grid;
@@ -563,21 +572,28 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   p.cb = 1;
   while (p.cb < 32 && (1ull << p.cb) <= Lmax) ++p.cb;
   p.packed = p.cb < 32 && (Lmax / k) < (1ull << (32 - p.cb));
-  SSLayout Ls = ss_layout(k, kb, 4, p.packed);
-  p.gstate = Ls.total > SS_SMEM_STATE_MAX || 2ull * Ls.NB >= 0xffffull || k >= 0xffffu;
+  // 16-bit entries: the slot field's all-ones value must exceed k - 1
+  uint32_t sb = 1;
+  while ((1u << sb) - 1u < k) ++sb;
+  SSLayout Ls = ss_layout(k, kb, 2, p.packed);
+  p.gstate = k > SS_K_SMALL || Ls.total > SS_SMEM_STATE_MAX;
   if (!p.gstate) {
+    p.sb = sb;
+    p.fmask = (1u << (16 - sb)) - 1u;
     p.L = Ls;
     p.smem = SS_RING_BYTES + 64 + Ls.total;
     int nb;
     if (p.packed)
-      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint32_t, false, true>(p.smem)
-                   : ss_blocks_per_sm<uint64_t, uint32_t, false, true>(p.smem);
+      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(p.smem)
+                   : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(p.smem);
     else
-      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint32_t, false, false>(p.smem)
-                   : ss_blocks_per_sm<uint64_t, uint32_t, false, false>(p.smem);
+      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(p.smem)
+                   : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(p.smem);
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)nb * d.sms);
   } else {
     p.packed = false;
+    p.sb = 32;
+    p.fmask = 0xffffffffu;
     p.L = ss_layout(k, kb, 8, false);
     p.smem = SS_RING_BYTES + 64;
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
@@ -621,19 +637,21 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.o_T = p.L.T;
   a.NB = p.L.NB;
   a.cb = p.cb;
+  a.sb = p.sb;
+  a.fmask = p.fmask;
   cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   if (!p.gstate) {
     if (p.packed) {
       if (kb == 4)
-        ss_summarize_kernel<uint32_t, uint32_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint32_t, uint16_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
       else
-        ss_summarize_kernel<uint64_t, uint32_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint64_t, uint16_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
     } else {
       if (kb == 4)
-        ss_summarize_kernel<uint32_t, uint32_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint32_t, uint16_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
       else
-        ss_summarize_kernel<uint64_t, uint32_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint64_t, uint16_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
     }
   } else {
     if (kb == 4)

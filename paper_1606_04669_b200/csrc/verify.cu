@@ -2,31 +2,86 @@
 // can be used to determine the actual frequent items") and the final k-majority report
 // (PAPER.md:47, :80).
 //
-// K4 streams A once with 128-bit read-only loads. Every CTA indexes the candidate list in a
-// shared-memory hash table (key -> candidate index, linear probing, load <= 1/2) and counts hits
-// with shared-memory atomics; per-CTA counts are flushed into 64-bit global accumulators at the
-// end. Candidate lists too large for shared memory use one global table built by the setup
-// kernel. K5 keeps the candidates whose exact count reaches floor(n/k) + 1 and ranks them by
-// (count desc, item asc).
+// K4 streams A once with 128-bit read-only loads, software-pipelined (the next loads are in flight
+// while the current ones are counted). The candidate list is a static set, so a setup kernel
+// builds a two-choice cuckoo table (key, candidate index) sized for the actual number of
+// candidates; every CTA copies it to shared memory and each item is looked up with two
+// independent loads and no probing loop. Counting, by the candidate count nc (decided on the
+// device, as nc is only known there):
+//   - small nc: every lane owns a private 16-bit counter per candidate, laid out [cand][lane] so
+//     a warp's increments hit 32 different banks: no atomics, no grouping;
+//   - larger nc: equal indices of a warp instruction are grouped with __match_any_sync and the
+//     leader adds the group size to a per-warp 32-bit counter;
+//   - beyond shared memory: the same grouping with 64-bit global atomics.
+// Per-CTA sums are flushed into 64-bit global accumulators at the end. K5 keeps the candidates
+// whose exact count reaches floor(n/k) + 1 and ranks them by (count desc, item asc).
 #include "common.cuh"
 
 namespace pss {
 
-constexpr uint32_t VT_LOG_MAX = 11;  // shared-memory table: up to 2048 entries, n_cand <= 1024
-constexpr int VTHREADS = 512;
+constexpr int VTHREADS = 128;
+constexpr int VWARPS = VTHREADS / 32;
+constexpr uint32_t VT_SMEM = 1024;       // table entries staged in shared memory
+constexpr uint32_t VC_BYTES = 32 * 1024; // shared-memory counter area per CTA
+constexpr uint32_t VLANE_MAX = VC_BYTES / (VWARPS * 32 * 2);  // nc for per-lane 16-bit counters
+constexpr uint32_t VWARP_MAX = VC_BYTES / (VWARPS * 4);       // nc for per-warp 32-bit counters
+
+// table entry: (key, candidate index); index all-ones = empty
+template <typename KT>
+struct VEnt;
+template <>
+struct VEnt<uint32_t> {
+  using T = unsigned long long;  // idx << 32 | key
+  __device__ static __forceinline__ T make(uint32_t key, uint32_t idx) {
+    return ((T)idx << 32) | key;
+  }
+  __device__ static __forceinline__ uint32_t key(T e) { return (uint32_t)e; }
+  __device__ static __forceinline__ uint32_t idx(T e) { return (uint32_t)(e >> 32); }
+  __device__ static __forceinline__ bool empty(T e) { return (uint32_t)(e >> 32) == 0xffffffffu; }
+  __device__ static __forceinline__ T none() { return ~0ull; }
+};
+template <>
+struct VEnt<uint64_t> {
+  using T = ulonglong2;  // {key, idx}
+  __device__ static __forceinline__ T make(uint64_t key, uint32_t idx) {
+    return make_ulonglong2(key, idx);
+  }
+  __device__ static __forceinline__ uint64_t key(T e) { return e.x; }
+  __device__ static __forceinline__ uint32_t idx(T e) { return (uint32_t)e.y; }
+  __device__ static __forceinline__ bool empty(T e) { return e.y == ~0ull; }
+  __device__ static __forceinline__ T none() { return make_ulonglong2(0ull, ~0ull); }
+};
+
+__device__ __forceinline__ uint32_t vfold(uint32_t x) { return x; }
+__device__ __forceinline__ uint32_t vfold(uint64_t x) {
+  return (uint32_t)((x * 0x9E3779B97F4A7C15ull) >> 32) ^ (uint32_t)x;
+}
+template <typename KT>
+__device__ __forceinline__ void vhash(KT x, uint32_t seed, uint32_t logT, uint32_t& h1,
+                                      uint32_t& h2) {
+  const uint32_t a = vfold(x) ^ seed;
+  const uint32_t ha = a * 0x9E3779B1u;
+  const uint32_t hb = (ha ^ (ha >> 15)) * 0x85EBCA6Bu;
+  h1 = ha >> (32u - logT);
+  h2 = hb >> (32u - logT);
+  h2 = h2 == h1 ? (h2 ^ 1u) : h2;  // two distinct entries per key
+}
+
+__host__ __device__ static uint32_t v_logT(uint32_t nc) {
+  uint32_t l = ceil_log2(4ull * (nc ? nc : 1));
+  return l < 6 ? 6 : l;
+}
 
 struct VLayout {
-  size_t acc, gkeys, gidx, total;
-  uint32_t logT;
+  size_t acc, tab, ctl, total;
 };
 
 static VLayout v_layout(int kb, uint32_t cap) {
   VLayout L;
-  L.logT = ceil_log2(2ull * (cap ? cap : 1));
   Bump b;
   L.acc = b.take<unsigned long long>(cap ? cap : 1);
-  L.gkeys = b.take<unsigned char>(((size_t)1 << L.logT) * kb);
-  L.gidx = b.take<uint32_t>((size_t)1 << L.logT);
+  L.tab = b.take<unsigned char>(((size_t)1 << v_logT(cap)) * (kb == 4 ? 8 : 16));
+  L.ctl = b.take<uint32_t>(4);  // [0] seed, [1] logT
   L.total = b.bytes();
   return L;
 }
@@ -35,81 +90,123 @@ __device__ __forceinline__ uint32_t eff_count(uint32_t cap, const uint32_t* d_n)
   return d_n ? min(cap, *d_n) : cap;
 }
 
-// insert candidate j into a table (duplicates may be inserted twice; lookups always see the
-// first copy on the probe path, so counting stays consistent)
+// candidate index of x in the table, or 0xffffffff
 template <typename KT>
-__device__ __forceinline__ void vt_insert(KT* tk, uint32_t* ti, uint32_t logT, KT x, uint32_t j) {
-  const uint32_t mask = (1u << logT) - 1u;
-  uint32_t h = hslot(x, logT);
-  while (atomicCAS(&ti[h], 0xffffffffu, j) != 0xffffffffu) h = (h + 1u) & mask;
-  tk[h] = x;
+__device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT x, uint32_t seed,
+                                            uint32_t logT) {
+  uint32_t h1, h2;
+  vhash(x, seed, logT, h1, h2);
+  const typename VEnt<KT>::T a = tab[h1];
+  const typename VEnt<KT>::T b = tab[h2];
+  const uint32_t ia = (!VEnt<KT>::empty(a) && VEnt<KT>::key(a) == x) ? VEnt<KT>::idx(a) : 0xffffffffu;
+  const uint32_t ib = (!VEnt<KT>::empty(b) && VEnt<KT>::key(b) == x) ? VEnt<KT>::idx(b) : 0xffffffffu;
+  return min(ia, ib);
 }
 
-template <typename KT>
-__device__ __forceinline__ int32_t vt_find(const KT* tk, const uint32_t* ti, uint32_t logT, KT x) {
-  const uint32_t mask = (1u << logT) - 1u;
-  uint32_t h = hslot(x, logT);
-  while (true) {
-    const uint32_t j = ti[h];
-    if (j == 0xffffffffu) return -1;
-    if (tk[h] == x) return (int32_t)h;
-    h = (h + 1u) & mask;
-  }
-}
-
+// builds the cuckoo table of the (deduplicated) candidates, sized for the actual count; zeroes
+// the accumulators
 template <typename KT>
 __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t* d_n,
-                                    unsigned long long* acc, KT* gk, uint32_t* gi,
-                                    uint32_t logTcap) {
+                                    unsigned long long* acc, typename VEnt<KT>::T* tab,
+                                    uint32_t* ctl) {
+  using VT = typename VEnt<KT>::T;
   const uint32_t nc = eff_count(cap, d_n);
-  for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
-  const uint32_t logT = ceil_log2(2ull * (nc ? nc : 1));
-  if (logT <= VT_LOG_MAX) return;  // shared-memory tables are built per CTA
+  const uint32_t logT = v_logT(nc);
   const uint32_t T = 1u << logT;
-  for (uint32_t h = threadIdx.x; h < T; h += blockDim.x) gi[h] = 0xffffffffu;
+  for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
+  for (uint32_t h = threadIdx.x; h < T; h += blockDim.x) tab[h] = VEnt<KT>::none();
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) vt_insert(gk, gi, logT, cand[j], j);
-  (void)logTcap;
-}
-
-template <typename KT>
-__device__ __forceinline__ void count_item(KT x, const KT* tk, const uint32_t* ti, uint32_t logT,
-                                           uint32_t* scnt, unsigned long long* acc, bool gl) {
-  const int32_t h = vt_find(tk, ti, logT, x);
-  if (h >= 0) {
-    if (gl)
-      atomicAdd(&acc[ti[h]], 1ull);
-    else
-      atomicAdd(&scnt[h], 1u);
+  if (threadIdx.x != 0) return;
+  for (uint32_t seed = 0;; seed += 0x9E3779B9u) {
+    if (seed)
+      for (uint32_t h = 0; h < T; ++h) tab[h] = VEnt<KT>::none();
+    bool ok = true;
+    for (uint32_t j = 0; j < nc && ok; ++j) {
+      KT x = cand[j];
+      if (vlookup<KT>(tab, x, seed, logT) != 0xffffffffu) continue;  // duplicate: first wins
+      uint32_t idx = j;
+      uint32_t prev = 0xffffffffu;
+      ok = false;
+      for (int step = 0; step < 500; ++step) {
+        uint32_t h1, h2;
+        vhash(x, seed, logT, h1, h2);
+        if (VEnt<KT>::empty(tab[h1])) {
+          tab[h1] = VEnt<KT>::make(x, idx);
+          ok = true;
+          break;
+        }
+        if (VEnt<KT>::empty(tab[h2])) {
+          tab[h2] = VEnt<KT>::make(x, idx);
+          ok = true;
+          break;
+        }
+        const uint32_t h = (h1 != prev) ? h1 : h2;
+        const VT e = tab[h];
+        tab[h] = VEnt<KT>::make(x, idx);
+        x = VEnt<KT>::key(e);
+        idx = VEnt<KT>::idx(e);
+        prev = h;
+      }
+    }
+    if (ok) {
+      ctl[0] = seed;
+      ctl[1] = logT;
+      return;
+    }
   }
 }
 
+// lane_ok: per-lane 16-bit counters cannot overflow for this launch (host-checked)
 template <typename KT>
 __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__ A, uint64_t n,
-                                                          const KT* cand, uint32_t cap,
-                                                          const uint32_t* d_n,
-                                                          unsigned long long* acc, const KT* gk,
-                                                          const uint32_t* gi) {
-  __shared__ KT tk_s[1u << VT_LOG_MAX];
-  __shared__ uint32_t ti_s[1u << VT_LOG_MAX];
-  __shared__ uint32_t scnt[1u << VT_LOG_MAX];
+                                                          uint32_t cap, const uint32_t* d_n,
+                                                          unsigned long long* acc,
+                                                          const typename VEnt<KT>::T* gtab,
+                                                          const uint32_t* ctl, uint32_t lane_ok) {
+  using VT = typename VEnt<KT>::T;
+  extern __shared__ __align__(16) unsigned char vsm[];
   const uint32_t nc = eff_count(cap, d_n);
   if (nc == 0) return;
-  const uint32_t logT = ceil_log2(2ull * nc);
-  const bool gl = logT > VT_LOG_MAX;
-  const KT* tk = gl ? gk : tk_s;
-  const uint32_t* ti = gl ? gi : ti_s;
-  if (!gl) {
-    const uint32_t T = 1u << logT;
-    for (uint32_t h = threadIdx.x; h < T; h += VTHREADS) {
-      ti_s[h] = 0xffffffffu;
-      scnt[h] = 0;
+  const uint32_t seed = ctl[0], logT = ctl[1];
+  const uint32_t T = 1u << logT;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
+  const int mode = (lane_ok && nc <= VLANE_MAX) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
+  VT* stab = reinterpret_cast<VT*>(vsm);
+  unsigned char* carea = vsm + (size_t)VT_SMEM * sizeof(VT);
+  uint16_t* lc = reinterpret_cast<uint16_t*>(carea) + (size_t)warp * nc * 32;  // [cand][lane]
+  uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;       // [cand]
+  const bool tab_smem = T <= VT_SMEM;
+  if (tab_smem)
+    for (uint32_t h = threadIdx.x; h < T; h += VTHREADS) stab[h] = gtab[h];
+  if (mode == 0)
+    for (uint32_t i = threadIdx.x; i < VWARPS * nc * 32; i += VTHREADS)
+      reinterpret_cast<uint16_t*>(carea)[i] = 0;
+  else if (mode == 1)
+    for (uint32_t i = threadIdx.x; i < VWARPS * nc; i += VTHREADS)
+      reinterpret_cast<uint32_t*>(carea)[i] = 0;
+  __syncthreads();
+  const VT* tab = tab_smem ? stab : gtab;
+
+  // count the candidate indices j[0..NJ) of one step of the warp
+  auto count = [&](const uint32_t* j, int NJ) {
+    if (mode == 0) {
+      for (int t = 0; t < NJ; ++t)
+        if (j[t] != 0xffffffffu) lc[j[t] * 32 + lane] += 1;
+    } else {
+      const uint32_t ltm = lanemask_lt();
+      for (int t = 0; t < NJ; ++t) {
+        const uint32_t g = __match_any_sync(PSS_FULL, j[t]);
+        if ((g & ltm) == 0 && j[t] != 0xffffffffu) {
+          if (mode == 1)
+            wc[j[t]] += __popc(g);
+          else
+            atomicAdd(&acc[j[t]], (unsigned long long)__popc(g));
+        }
+      }
     }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < nc; j += VTHREADS) vt_insert(tk_s, ti_s, logT, cand[j], j);
-    __syncthreads();
-  }
-  // head items before the first 16-byte boundary, then 16-byte vectors, then the tail
+  };
+
   constexpr uint32_t E = 16 / sizeof(KT);
   const uintptr_t addr = reinterpret_cast<uintptr_t>(A);
   uint64_t head = ((16u - (addr & 15u)) & 15u) / sizeof(KT);
@@ -117,48 +214,78 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   if (head > n) head = n;
   const uint64_t nvec = (n - head) / E;
   const uint64_t tail0 = head + nvec * E;
-  const uint64_t gtid = (uint64_t)blockIdx.x * VTHREADS + threadIdx.x;
-  const uint64_t gstride = (uint64_t)gridDim.x * VTHREADS;
-  for (uint64_t i = gtid; i < head; i += gstride) count_item(A[i], tk, ti, logT, scnt, acc, gl);
+  const uint64_t wid = (uint64_t)blockIdx.x * VWARPS + warp;
+  const uint64_t nwarps = (uint64_t)gridDim.x * VWARPS;
+  // scalar head and tail (warp-uniform loops)
+  for (uint64_t base = wid * 32; base < head; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    uint32_t j = i < head ? vlookup<KT>(tab, A[i], seed, logT) : 0xffffffffu;
+    count(&j, 1);
+  }
   const uint4* V = reinterpret_cast<const uint4*>(A + head);
-  uint64_t v = gtid;
-  for (; v + gstride < nvec; v += 2 * gstride) {  // two 16-byte loads in flight per thread
-    const uint4 q0 = __ldg(V + v);
-    const uint4 q1 = __ldg(V + v + gstride);
-    const KT* x0 = reinterpret_cast<const KT*>(&q0);
-    const KT* x1 = reinterpret_cast<const KT*>(&q1);
+  const uint64_t stride = nwarps * 32;
+  // software pipeline over U 16-byte loads per lane; all lanes of a warp take the same trip count
+  constexpr int U = 4;
+  uint4 q[U], nq[U];
+  uint64_t vb = wid * 32;
 #pragma unroll
-    for (uint32_t e = 0; e < E; ++e) count_item(x0[e], tk, ti, logT, scnt, acc, gl);
-#pragma unroll
-    for (uint32_t e = 0; e < E; ++e) count_item(x1[e], tk, ti, logT, scnt, acc, gl);
+  for (int u = 0; u < U; ++u) {
+    const uint64_t va = vb + u * stride + lane;
+    q[u] = va < nvec ? __ldg(V + va) : make_uint4(0, 0, 0, 0);
   }
-  for (; v < nvec; v += gstride) {
-    const uint4 q0 = __ldg(V + v);
-    const KT* x0 = reinterpret_cast<const KT*>(&q0);
+  for (; vb < nvec; vb += U * stride) {
+    bool ok[U];
 #pragma unroll
-    for (uint32_t e = 0; e < E; ++e) count_item(x0[e], tk, ti, logT, scnt, acc, gl);
+    for (int u = 0; u < U; ++u) {
+      ok[u] = vb + u * stride + lane < nvec;
+      const uint64_t vn = vb + (U + u) * stride + lane;
+      nq[u] = vn < nvec ? __ldg(V + vn) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t j[U * E];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const KT* xs = reinterpret_cast<const KT*>(&q[u]);
+#pragma unroll
+      for (uint32_t e = 0; e < E; ++e)
+        j[u * E + e] = ok[u] ? vlookup<KT>(tab, xs[e], seed, logT) : 0xffffffffu;
+    }
+    count(j, U * E);
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = nq[u];
   }
-  for (uint64_t i = tail0 + gtid; i < n; i += gstride) count_item(A[i], tk, ti, logT, scnt, acc, gl);
-  if (!gl) {
+  for (uint64_t base = tail0 + wid * 32; base < n; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    uint32_t j = i < n ? vlookup<KT>(tab, A[i], seed, logT) : 0xffffffffu;
+    count(&j, 1);
+  }
+  if (mode != 2) {
     __syncthreads();
-    const uint32_t T = 1u << logT;
-    for (uint32_t h = threadIdx.x; h < T; h += VTHREADS)
-      if (scnt[h]) atomicAdd(&acc[ti_s[h]], (unsigned long long)scnt[h]);
+    for (uint32_t c = threadIdx.x; c < nc; c += VTHREADS) {
+      unsigned long long t = 0;
+      if (mode == 0) {
+        const uint16_t* base = reinterpret_cast<const uint16_t*>(carea);
+        for (uint32_t w = 0; w < VWARPS; ++w)
+          for (uint32_t l = 0; l < 32; ++l) t += base[((size_t)w * nc + c) * 32 + l];
+      } else {
+        const uint32_t* base = reinterpret_cast<const uint32_t*>(carea);
+        for (uint32_t w = 0; w < VWARPS; ++w) t += base[(size_t)w * nc + c];
+      }
+      if (t) atomicAdd(&acc[c], t);
+    }
   }
 }
 
-// exact[j] = sum of acc over all candidate positions holding cand[j] (duplicates share counts)
+// exact[j] = the count accumulated for the first position holding cand[j] (duplicates share it)
 template <typename KT>
 __global__ void verify_finalize_kernel(const KT* cand, uint32_t cap, const uint32_t* d_n,
-                                       const unsigned long long* acc, uint64_t* exact) {
+                                       const unsigned long long* acc,
+                                       const typename VEnt<KT>::T* tab, const uint32_t* ctl,
+                                       uint64_t* exact) {
   const uint32_t nc = eff_count(cap, d_n);
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
-  const KT x = cand[j];
-  uint64_t t = 0;
-  for (uint32_t i = 0; i < nc; ++i)
-    if (cand[i] == x) t += acc[i];
-  exact[j] = t;
+  const uint32_t f = vlookup<KT>(tab, cand[j], ctl[0], ctl[1]);
+  exact[j] = acc[f];
 }
 
 size_t verify_ws(int kb, uint32_t cap, const DevInfo&) { return v_layout(kb, cap).total; }
@@ -167,20 +294,26 @@ template <typename KT>
 static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t cap,
                               const uint32_t* d_n, uint64_t* exact, void* ws, cudaStream_t s,
                               const DevInfo& d) {
+  using VT = typename VEnt<KT>::T;
   VLayout L = v_layout(sizeof(KT), cap);
   unsigned char* w = static_cast<unsigned char*>(ws);
   auto* acc = reinterpret_cast<unsigned long long*>(w + L.acc);
-  auto* gk = reinterpret_cast<KT*>(w + L.gkeys);
-  auto* gi = reinterpret_cast<uint32_t*>(w + L.gidx);
+  auto* tab = reinterpret_cast<VT*>(w + L.tab);
+  auto* ctl = reinterpret_cast<uint32_t*>(w + L.ctl);
   if (cap == 0) return cudaSuccess;
-  verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, gk, gi, L.logT);
+  verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, ctl);
+  const size_t smem = (size_t)VT_SMEM * sizeof(VT) + VC_BYTES;
+  cudaFuncSetAttribute(verify_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<KT>, VTHREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<KT>, VTHREADS, smem);
   if (nb < 1) nb = 1;
-  const uint64_t want = (n + (uint64_t)VTHREADS * 16 - 1) / ((uint64_t)VTHREADS * 16);
+  const uint64_t want = (n + (uint64_t)VTHREADS * 64 - 1) / ((uint64_t)VTHREADS * 64);
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nb * d.sms));
-  verify_kernel<KT><<<grid, VTHREADS, 0, s>>>(A, n, cand, cap, d_n, acc, gk, gi);
-  verify_finalize_kernel<KT><<<(cap + 255) / 256, 256, 0, s>>>(cand, cap, d_n, acc, exact);
+  // items one lane counts: at most ceil(n / (grid * VTHREADS)) + the head/tail
+  const uint64_t per_lane = n / ((uint64_t)grid * VTHREADS) + 64;
+  const uint32_t lane_ok = per_lane < 65535u;
+  verify_kernel<KT><<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, ctl, lane_ok);
+  verify_finalize_kernel<KT><<<(cap + 255) / 256, 256, 0, s>>>(cand, cap, d_n, acc, tab, ctl, exact);
   return cudaGetLastError();
 }
 

@@ -209,6 +209,12 @@ def test_verify_duplicates_absent_and_device_count(pss):
     ex3 = pss.pss_verify(dA, to_dev(many))
     torch.cuda.synchronize()
     assert ex3.cpu().numpy().tolist() == oracle.verify(A, many).tolist()
+    # the three counting modes: per-lane counters, per-warp grouped counters, global atomics
+    for nc in (1, 128, 129, 500, 2048, 2049):
+        c = np.unique(A)[:nc]
+        ex4 = pss.pss_verify(dA, to_dev(c))
+        torch.cuda.synchronize()
+        assert ex4.cpu().numpy().tolist() == oracle.verify(A, c).tolist(), nc
 
 
 def test_query_host_end_to_end(pss):
