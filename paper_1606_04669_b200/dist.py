@@ -49,8 +49,8 @@ def gather_summaries(root: Summaries, group=None) -> Summaries:
                     torch.empty((world,), dtype=root.sizes.dtype, device=root.items.device))
     for src, dst in ((root.items, out.items), (root.counts, out.counts), (root.errs, out.errs),
                      (root.sizes, out.sizes)):
-        dist.all_gather_into_tensor(_as_signed(dst).view(-1), _as_signed(src).reshape(-1),
-                                    group=group)
+        parts = list(_as_signed(dst).reshape(world, -1).unbind(0))
+        dist.all_gather(parts, _as_signed(src).reshape(-1), group=group)
     return out
 
 
