@@ -23,7 +23,7 @@ __all__ = ["Summaries", "PssError", "pss_workspace_bytes", "pss_summarize", "pss
            "EXPORTED_SYMBOLS"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_PKG, "libpss.so")
+lib_path = os.environ.get("PSS_LIB") or os.path.join(_PKG, "libpss.so")  # PSS_LIB: dev builds
 
 KEY_U32, KEY_U64 = 0, 1
 OP_SUMMARIZE, OP_MERGE, OP_COMBINE, OP_VERIFY, OP_QUERY = range(5)

@@ -55,7 +55,7 @@ namespace pss {
   } while (0)
 #endif
 
-constexpr uint32_t SS_RING_BYTES = 2048;  // per-warp TMA ring
+constexpr uint32_t SS_RING_BYTES = 2048;  // per-warp TMA ring (4 stages of 512 bytes)
 constexpr uint32_t SS_NSTAGE = 4;
 constexpr uint32_t SS_STAGE_BYTES = SS_RING_BYTES / SS_NSTAGE;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
@@ -442,7 +442,11 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
         const KT x = ring[(roff + q + lane) & RMASK];
+#ifdef PSS_EXP_MATCH2  // timing experiment only (tools/variant.sh): a second, redundant match
+        const uint32_t grp = __match_any_sync(PSS_FULL, x) & __match_any_sync(PSS_FULL, x + 1) & amask;
+#else
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
+#endif
 
         // victims for this step (independent of the lookups): lane j holds the j-th next slot
         // of B_m at or after the cursor (two bitmap words) and the index entry of its item
@@ -582,6 +586,8 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     p.fmask = (1u << (16 - sb)) - 1u;
     p.L = Ls;
     p.smem = SS_RING_BYTES + 64 + Ls.total;
+    if (const char* pad = std::getenv("PSS_DEBUG_SMEM_PAD"))  // experiment hook: fewer warps/SM
+      p.smem += (size_t)std::atoll(pad);
     int nb;
     if (p.packed)
       nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(p.smem)
