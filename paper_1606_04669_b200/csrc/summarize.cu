@@ -238,13 +238,17 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       for (int step = 0; step < SS_MAX_KICKS; ++step) {
         uint32_t b1, b2, fp;
         key_hash<ET>(en, cx, seed, NB, b1, b2, fp);
-        const uint32_t cand[4] = {2 * b1, 2 * b1 + 1, 2 * b2, 2 * b2 + 1};
-        for (int j = 0; j < 4; ++j) {
-          if (T[cand[j]] == EMPTY) {
-            T[cand[j]] = en.make(fp, cv);
-            pos[cv] = (PT)cand[j];
-            return true;
-          }
+        ET f0, f1, f2, f3;
+        load_bucket(T, b1, f0, f1);
+        load_bucket(T, b2, f2, f3);
+        uint32_t fi = f3 == EMPTY ? 2 * b2 + 1 : 0xffffffffu;
+        fi = f2 == EMPTY ? 2 * b2 : fi;
+        fi = f1 == EMPTY ? 2 * b1 + 1 : fi;
+        fi = f0 == EMPTY ? 2 * b1 : fi;
+        if (fi != 0xffffffffu) {
+          T[fi] = en.make(fp, cv);
+          pos[cv] = (PT)fi;
+          return true;
         }
         const uint32_t kb = (b1 != prev) ? b1 : b2;
         const uint32_t idx = 2 * kb + ((step ^ (cv & 1)) & 1);
