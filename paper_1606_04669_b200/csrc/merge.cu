@@ -9,6 +9,8 @@
 // a bitonic network over NT threads x EPT elements held in registers: exchanges between elements
 // of one thread stay in registers, exchanges within a warp use shuffles, and only the strides of
 // 32*EPT elements and more go through shared memory. Outputs are in canonical order.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pss {
@@ -470,7 +472,10 @@ static MPlan m_plan(int kb, uint32_t k, const DevInfo& d) {
   MPlan p;
   uint32_t NP = 1u << ceil_log2(2ull * k);
   if (NP < 256) NP = 256;
-  p.nt = (int)std::min<uint32_t>(1024, NP / 2);
+  const char* nts = std::getenv("PSS_DEBUG_MERGE_NT");  // experiment hook
+  const uint32_t ntmax = nts ? (uint32_t)std::atoi(nts) : 512u;
+  p.nt = (int)std::min<uint32_t>(ntmax, NP / 2);
+  if (NP / p.nt > 8) p.nt = (int)std::min<uint32_t>(1024, NP / 2);
   p.ept = (int)(NP / p.nt);
   p.L = m_layout(k, kb, NP);
   p.g = p.L.total > (size_t)d.smem_optin - 2048;
@@ -492,6 +497,10 @@ static bool dispatch_comb(const CombArgs& a, int grid, const MPlan& p, cudaStrea
     case 128 * 100 + 2: launch_comb<KT, G, 128, 2>(a, grid, p.smem, s); return true;
     case 256 * 100 + 2: launch_comb<KT, G, 256, 2>(a, grid, p.smem, s); return true;
     case 512 * 100 + 2: launch_comb<KT, G, 512, 2>(a, grid, p.smem, s); return true;
+    case 512 * 100 + 4: launch_comb<KT, G, 512, 4>(a, grid, p.smem, s); return true;
+    case 512 * 100 + 8: launch_comb<KT, G, 512, 8>(a, grid, p.smem, s); return true;
+    case 256 * 100 + 4: launch_comb<KT, G, 256, 4>(a, grid, p.smem, s); return true;
+    case 256 * 100 + 8: launch_comb<KT, G, 256, 8>(a, grid, p.smem, s); return true;
     case 1024 * 100 + 2: launch_comb<KT, G, 1024, 2>(a, grid, p.smem, s); return true;
     case 1024 * 100 + 4: launch_comb<KT, G, 1024, 4>(a, grid, p.smem, s); return true;
     case 1024 * 100 + 8: launch_comb<KT, G, 1024, 8>(a, grid, p.smem, s); return true;
