@@ -21,7 +21,7 @@ namespace pss {
 
 constexpr int VTHREADS = 128;
 constexpr int VWARPS = VTHREADS / 32;
-constexpr uint32_t VT_SMEM = 1024;       // table entries staged in shared memory
+constexpr uint32_t VT_SMEM = 2048;       // table entries staged in shared memory
 constexpr uint32_t VC_BYTES = 32 * 1024; // shared-memory counter area per CTA
 constexpr uint32_t VLANE_MAX = VC_BYTES / (VWARPS * 32 * 2);  // nc for per-lane 16-bit counters
 constexpr uint32_t VWARP_MAX = VC_BYTES / (VWARPS * 4);       // nc for per-warp 32-bit counters
@@ -76,12 +76,17 @@ struct VLayout {
   size_t acc, tab, ctl, total;
 };
 
+// perfect (collision-free, one probe) tables for up to PH_MAX distinct candidates
+constexpr uint32_t PH_MAX = 80;
+constexpr uint32_t PH_LOG = 11;  // 2048 entries
+constexpr int PH_TRIES = 64;
+
 static VLayout v_layout(int kb, uint32_t cap) {
   VLayout L;
   Bump b;
   L.acc = b.take<unsigned long long>(cap ? cap : 1);
-  L.tab = b.take<unsigned char>(((size_t)1 << v_logT(cap)) * (kb == 4 ? 8 : 16));
-  L.ctl = b.take<uint32_t>(4);  // [0] seed, [1] logT
+  L.tab = b.take<unsigned char>(((size_t)1 << std::max(v_logT(cap), PH_LOG)) * (kb == 4 ? 8 : 16));
+  L.ctl = b.take<uint32_t>(4);  // [0] seed, [1] logT, [2] 1 = perfect table
   L.total = b.bytes();
   return L;
 }
@@ -90,17 +95,23 @@ __device__ __forceinline__ uint32_t eff_count(uint32_t cap, const uint32_t* d_n)
   return d_n ? min(cap, *d_n) : cap;
 }
 
-// candidate index of x in the table, or 0xffffffff
+// candidate index of x in the table, or 0xffffffff (perfect: one entry per key)
 template <typename KT>
 __device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT x, uint32_t seed,
-                                            uint32_t logT) {
+                                            uint32_t logT, bool perfect) {
   uint32_t h1, h2;
   vhash(x, seed, logT, h1, h2);
   const typename VEnt<KT>::T a = tab[h1];
-  const typename VEnt<KT>::T b = tab[h2];
   const uint32_t ia = (!VEnt<KT>::empty(a) && VEnt<KT>::key(a) == x) ? VEnt<KT>::idx(a) : 0xffffffffu;
+  if (perfect) return ia;
+  const typename VEnt<KT>::T b = tab[h2];
   const uint32_t ib = (!VEnt<KT>::empty(b) && VEnt<KT>::key(b) == x) ? VEnt<KT>::idx(b) : 0xffffffffu;
   return min(ia, ib);
+}
+template <typename KT>
+__device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT x, uint32_t seed,
+                                            uint32_t logT) {
+  return vlookup<KT>(tab, x, seed, logT, false);
 }
 
 // builds the cuckoo table of the (deduplicated) candidates, sized for the actual count; zeroes
@@ -111,12 +122,45 @@ __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t
                                     uint32_t* ctl) {
   using VT = typename VEnt<KT>::T;
   const uint32_t nc = eff_count(cap, d_n);
+  for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
+  // perfect table: find a seed under which the (distinct) candidates occupy distinct entries
+  __shared__ uint32_t occ[(1u << PH_LOG) / 32];
+  __shared__ uint32_t clash;
+  if (nc > 0 && nc <= PH_MAX) {
+    const uint32_t TP = 1u << PH_LOG;
+    for (int tr = 0; tr < PH_TRIES; ++tr) {
+      const uint32_t seed = (uint32_t)tr * 0x9E3779B9u + 0x7F4A7C15u;
+      for (uint32_t i = threadIdx.x; i < TP / 32; i += blockDim.x) occ[i] = 0;
+      if (threadIdx.x == 0) clash = 0;
+      __syncthreads();
+      uint32_t h = 0, h2;
+      if (threadIdx.x < nc) {
+        vhash(cand[threadIdx.x], seed, PH_LOG, h, h2);
+        const uint32_t old = atomicOr(&occ[h >> 5], 1u << (h & 31));
+        if (old & (1u << (h & 31))) clash = 1;  // also catches duplicate candidates
+      }
+      __syncthreads();
+      if (!clash) {
+        for (uint32_t e = threadIdx.x; e < TP; e += blockDim.x) tab[e] = VEnt<KT>::none();
+        __syncthreads();
+        if (threadIdx.x < nc) tab[h] = VEnt<KT>::make(cand[threadIdx.x], threadIdx.x);
+        if (threadIdx.x == 0) {
+          ctl[0] = seed;
+          ctl[1] = PH_LOG;
+          ctl[2] = 1;
+        }
+        return;
+      }
+      __syncthreads();
+    }
+  }
+  // two-choice cuckoo table (duplicates allowed: the first occurrence owns the entry)
   const uint32_t logT = v_logT(nc);
   const uint32_t T = 1u << logT;
-  for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
   for (uint32_t h = threadIdx.x; h < T; h += blockDim.x) tab[h] = VEnt<KT>::none();
   __syncthreads();
   if (threadIdx.x != 0) return;
+  ctl[2] = 0;
   for (uint32_t seed = 0;; seed += 0x9E3779B9u) {
     if (seed)
       for (uint32_t h = 0; h < T; ++h) tab[h] = VEnt<KT>::none();
@@ -168,6 +212,7 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint32_t nc = eff_count(cap, d_n);
   if (nc == 0) return;
   const uint32_t seed = ctl[0], logT = ctl[1];
+  const bool perf = ctl[2] != 0;
   const uint32_t T = 1u << logT;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
@@ -219,7 +264,7 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   // scalar head and tail (warp-uniform loops)
   for (uint64_t base = wid * 32; base < head; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    uint32_t j = i < head ? vlookup<KT>(tab, A[i], seed, logT) : 0xffffffffu;
+    uint32_t j = i < head ? vlookup<KT>(tab, A[i], seed, logT, perf) : 0xffffffffu;
     count(&j, 1);
   }
   const uint4* V = reinterpret_cast<const uint4*>(A + head);
@@ -247,7 +292,7 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
       const KT* xs = reinterpret_cast<const KT*>(&q[u]);
 #pragma unroll
       for (uint32_t e = 0; e < E; ++e)
-        j[u * E + e] = ok[u] ? vlookup<KT>(tab, xs[e], seed, logT) : 0xffffffffu;
+        j[u * E + e] = ok[u] ? vlookup<KT>(tab, xs[e], seed, logT, perf) : 0xffffffffu;
     }
     count(j, U * E);
 #pragma unroll
@@ -255,7 +300,7 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   }
   for (uint64_t base = tail0 + wid * 32; base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    uint32_t j = i < n ? vlookup<KT>(tab, A[i], seed, logT) : 0xffffffffu;
+    uint32_t j = i < n ? vlookup<KT>(tab, A[i], seed, logT, perf) : 0xffffffffu;
     count(&j, 1);
   }
   if (mode != 2) {
@@ -284,7 +329,7 @@ __global__ void verify_finalize_kernel(const KT* cand, uint32_t cap, const uint3
   const uint32_t nc = eff_count(cap, d_n);
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
-  const uint32_t f = vlookup<KT>(tab, cand[j], ctl[0], ctl[1]);
+  const uint32_t f = vlookup<KT>(tab, cand[j], ctl[0], ctl[1], ctl[2] != 0);
   exact[j] = acc[f];
 }
 
