@@ -110,13 +110,14 @@ __device__ __forceinline__ bool canon_before(uint32_t ca, KT ka, uint32_t cb, KT
 // ---- host-side bump allocator over a workspace
 struct Bump {
   size_t off = 0;
+  size_t al = 256;  // alignment of every region (16 is enough for shared-memory layouts)
   template <typename T>
   size_t take(size_t count) {
-    size_t o = align_up(off, 256);
+    size_t o = align_up(off, al);
     off = o + count * sizeof(T);
     return o;
   }
-  size_t bytes() const { return align_up(off, 256); }
+  size_t bytes() const { return align_up(off, al); }
 };
 
 // ---- internal launchers (csrc/*.cu) ----------------------------------------------------

@@ -55,12 +55,13 @@ namespace pss {
   } while (0)
 #endif
 
-constexpr uint32_t SS_RING_BYTES = 2048;  // per-warp TMA ring (4 stages of 512 bytes)
-constexpr uint32_t SS_NSTAGE = 4;
-constexpr uint32_t SS_STAGE_BYTES = SS_RING_BYTES / SS_NSTAGE;
+// per-warp TMA ring: 3 stages of 512 bytes (a step spans at most two stages; one more in flight)
+constexpr uint32_t SS_NSTAGE = 3;
+constexpr uint32_t SS_STAGE_BYTES = 512;
+constexpr uint32_t SS_RING_BYTES = SS_NSTAGE * SS_STAGE_BYTES;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
 constexpr uint32_t SS_K_SMALL = 4094;             // 16-bit index entries up to this k
-constexpr double SS_LOAD = 0.30;                  // index load factor (live keys / entries)
+constexpr double SS_LOAD = 0.32;                  // index load factor (live keys / entries)
 constexpr int SS_MAX_KICKS = 200;
 
 // Index entry layout (runtime): slot in the low sb bits, fingerprint above. A slot field of all
@@ -133,10 +134,11 @@ static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed) {
   const size_t KP = align_up(k, 32);
   L.NB = (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * ss_load())));
   Bump b;
-  L.keys = b.take<unsigned char>(KP * kb);
-  L.cnt = b.take<uint32_t>(KP);
-  L.err = packed ? L.cnt : b.take<uint32_t>(KP);
-  L.pos = b.take<unsigned char>(KP * (eb == 2 ? 2 : 4));
+  b.al = 16;  // every slot-indexed array holds exactly k entries (slots are < k)
+  L.keys = b.take<unsigned char>((size_t)k * kb);
+  L.cnt = b.take<uint32_t>(k);
+  L.err = packed ? L.cnt : b.take<uint32_t>(k);
+  L.pos = b.take<unsigned char>((size_t)k * (eb == 2 ? 2 : 4));
   L.bm = b.take<uint32_t>(KP / 32 + 2);
   L.vic = b.take<uint32_t>(32);
   L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   const uint32_t lane = threadIdx.x;
   const uint32_t ltm = lanemask_lt();
   constexpr uint32_t ST = SS_STAGE_BYTES / sizeof(KT);  // items per stage
-  constexpr uint32_t RMASK = SS_NSTAGE * ST - 1;
+  constexpr uint32_t RING = SS_NSTAGE * ST;  // ring capacity in items
   constexpr uint32_t E = 16 / sizeof(KT);  // items per 16 bytes
   constexpr ET EMPTY = Ent<ET>::EMPTY;
   const Ent<ET> en{a.sb, a.fmask};
@@ -178,8 +180,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + 64;
   KT* keys = reinterpret_cast<KT*>(st);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);  // count (| err << cb if PACKED)
+  PT* pos = reinterpret_cast<PT*>(st + a.o_pos);               // index entry of each slot
   uint32_t* err = reinterpret_cast<uint32_t*>(st + a.o_err);
-  PT* pos = reinterpret_cast<PT*>(st + a.o_pos);
   uint32_t* bm = reinterpret_cast<uint32_t*>(st + a.o_bm);
   uint32_t* vic = reinterpret_cast<uint32_t*>(st + a.o_vic);
   ET* T = reinterpret_cast<ET*>(st + a.o_T);
@@ -341,7 +343,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
             const uint32_t sl = ready % SS_NSTAGE;
             mbar_wait(&bars[sl], (phasebits >> sl) & 1u);
             phasebits ^= 1u << sl;
-            if (ready + 2 >= SS_NSTAGE - 1 && ready + 2 < total) issue(ready + 2);
+            // stage ready + NSTAGE - 2 goes into the slot of stage ready - 2 (consumed)
+            const uint32_t nx = ready + SS_NSTAGE - 2;
+            if (nx >= SS_NSTAGE - 1 && nx < total) issue(nx);
             ++ready;
             ready_end = min(L, ready * ST - roff);
           }
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         ensure(q + nv);
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = ring[(roff + q + lane) & RMASK];
+        const KT x = ring[(roff + q + lane) % RING];
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
         int32_t s;
         uint32_t ce, fi, fp;
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         ensure(q + nv);
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = ring[(roff + q + lane) & RMASK];
+        const KT x = ring[(roff + q + lane) % RING];
 #ifdef PSS_EXP_MATCH2  // timing experiment only (tools/variant.sh): a second, redundant match
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & __match_any_sync(PSS_FULL, x + 1) & amask;
 #else
