@@ -49,9 +49,21 @@ extern "C" int pss_debug_stats(unsigned long long* out, int reset) {
   return (int)cudaGetLastError();
 }
 namespace pss {
+// step-phase timing (debug build): wait for a value, then read the SM clock
+#define SS_TICK(acc, t, val)                                         \
+  do {                                                               \
+    uint32_t _d;                                                     \
+    asm volatile("mov.b32 %0, %1;" : "=r"(_d) : "r"((uint32_t)(val))); \
+    const long long _t = clock64() + (_d & 0);                       \
+    acc += _t - t;                                                   \
+    t = _t;                                                          \
+  } while (0)
 #else
 #define SS_STAT(i, v) \
   do {                \
+  } while (0)
+#define SS_TICK(acc, t, val) \
+  do {                       \
   } while (0)
 #endif
 
@@ -281,6 +293,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     auto insert_all = [&](bool ins, KT x, uint32_t v, uint32_t fi, uint32_t fp, uint32_t nslots) {
       const ET mine = en.make(fp, v);
       const bool tryfi = ins && fi != 0xffffffffu;
+      // lanes that picked the same free entry: write, then read back (a match instruction here
+      // measured 12 % slower: __match_any_sync is the costliest instruction of a step)
       ET* const tp = T + (tryfi ? fi : 0u);
       if (tryfi) *tp = mine;
       __syncwarp();
@@ -291,6 +305,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       SS_STAT(2, __popc(need));
       SS_STAT(10, __popc(__ballot_sync(PSS_FULL, ins && fi == 0xffffffffu)));
       if (need) {
+        __syncwarp();  // the serial inserts see every fast-path write and deletion
         bool failed = false;
         while (need) {
           const uint32_t l = __ffs(need) - 1;
@@ -444,9 +459,15 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       if (size == k) new_level();
 
       // ---- all k counters occupied: misses evict the lowest slots of B_m (R1)
+#ifdef PSS_STATS
+      long long tk = 0, ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0, ph5 = 0;
+#endif
       while (q < L) {
         const uint32_t nv = min(32u, L - q);
         ensure(q + nv);
+#ifdef PSS_STATS
+        tk = clock64();
+#endif
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
         const KT x = ring[(roff + q + lane) % RING];
@@ -455,6 +476,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 #else
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
 #endif
+        SS_TICK(ph1, tk, grp);
 
         // victims for this step (independent of the lookups): lane j holds the j-th next slot
         // of B_m at or after the cursor (two bitmap words) and the index entry of its item
@@ -474,6 +496,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         int32_t s;
         uint32_t ce, fi, fp;
         lookup(x, act, s, ce, fi, fp);
+        SS_TICK(ph2, tk, ce ^ (uint32_t)s ^ myop);
         const bool hit = s >= 0;
         const uint32_t cs = ce & CM;
         const bool leader = act && (grp & ltm) == 0;
@@ -505,6 +528,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
         const bool inpre = leader && lane < c;
         const uint32_t mult = __popc(grp & pm);
+        SS_TICK(ph3, tk, mult ^ vmax);
         // hits: count += multiplicity; a hit counter leaves B_m
         const bool hup = inpre && hit;
         const bool hitm = hup && cs == m;
@@ -528,6 +552,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
           if (!PACKED) err[v] = m;
         }
         insert_all(ev, x, v, fi, fp, size);
+        SS_TICK(ph4, tk, v);
         const uint32_t Mp = __popc(missL & pm);
         const uint32_t last = __shfl_sync(PSS_FULL, myvic, (Mp ? Mp : 1) - 1);
         if (Mp) cur = last + 1;
@@ -541,7 +566,15 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
           new_level();
         }
         __syncwarp();
+        SS_TICK(ph5, tk, bmcount);
       }
+#ifdef PSS_STATS
+      SS_STAT(11, ph1);
+      SS_STAT(12, ph2);
+      SS_STAT(13, ph3);
+      SS_STAT(14, ph4);
+      SS_STAT(15, ph5);
+#endif
     }
 
     // ---- dump the leaf in slot order

@@ -66,7 +66,9 @@ def main():
     lib.pss_debug_stats(st, 0)
     s = list(st)
     names = ["full_steps", "items", "slow_insert_lanes", "rehash", "amb_steps", "trunc_victims",
-             "trunc_hazard", "new_level", "fill_steps", "evictions", "no_free_entry_lanes"]
+             "trunc_hazard", "new_level", "fill_steps", "evictions", "no_free_entry_lanes",
+             "cyc_load_match", "cyc_victims_lookup", "cyc_decide", "cyc_apply_insert",
+             "cyc_tail"]
     full = max(1, s[0])
     print(f"workload {args.workload} n={n} k={k} P={P}")
     for i, nm in enumerate(names):
