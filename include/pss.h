@@ -165,6 +165,11 @@ pss_status pss_query(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, u
  * host, pinned recommended) to d_A (device, capacity n keys), runs pss_query, and copies the
  * result back to h_out_items (capacity k), h_out_counts (capacity k) and h_out_len (one uint32).
  * The d->h copies are enqueued on `stream`; the host buffers are valid after it is synchronised.
+ * Inputs of 64 MiB or more are copied in 16 chunks cut at partition boundaries (Alg. 1 l.3-4) on
+ * a private stream created and released inside the call; the leaves of each chunk are summarized
+ * on `stream` as soon as the chunk has landed, so only the last chunk's leaves, the merge tree
+ * and the verification pass follow the transfer. The copies start after the work already
+ * enqueued on `stream`. Result identical to the unpipelined call.
  */
 pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
                           uint32_t P, void* h_out_items, uint64_t* h_out_counts,

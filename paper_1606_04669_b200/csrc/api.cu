@@ -1,6 +1,7 @@
 // api.cu -- the C-ABI of libpss.so (include/pss.h): argument validation, workspace layout and
 // launch order. No torch types, no allocation, no global mutable state.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -168,7 +169,7 @@ pss_status pss_report(const void* d_cand, uint32_t n_cand, const uint32_t* d_n_c
                                    d_out_counts, d_out_len, stream));
 }
 
-static pss_status query_impl(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
+static pss_status tree_and_verify(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
                              unsigned char* w, const QLayout& L, cudaStream_t s,
                              const DevInfo& d) {
@@ -184,13 +185,33 @@ static pss_status query_impl(const void* d_A, uint64_t n, int kb, uint32_t k, ui
   uint32_t* nc = reinterpret_cast<uint32_t*>(w + L.ncand);
   uint64_t* exact = reinterpret_cast<uint64_t*>(w + L.exact);
   void* sc = w + L.scratch;
-  cudaError_t e = summarize_launch(d_A, n, kb, k, P, li, lc, le, ls, sc, s, d);
-  if (e == cudaSuccess) e = merge_tree_launch(kb, k, P, li, lc, le, ls, ri, rc, re, rs, sc, s, d);
+  cudaError_t e = merge_tree_launch(kb, k, P, li, lc, le, ls, ri, rc, re, rs, sc, s, d);
   if (e == cudaSuccess) e = prune_launch(kb, k, ri, rc, rs, n, cand, nc, s);
   if (e == cudaSuccess) e = verify_launch(d_A, n, kb, cand, k, nc, exact, sc, s, d);
   if (e == cudaSuccess)
     e = result_launch(kb, k, cand, nc, exact, n, k, d_out_items, d_out_counts, d_out_len, s);
   return cuda_status(e);
+}
+
+// a2 then a4..a7
+static pss_status query_impl(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
+                             void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                             unsigned char* w, const QLayout& L, cudaStream_t s,
+                             const DevInfo& d) {
+  const cudaError_t e = summarize_launch(
+      d_A, n, kb, k, P, w + L.l_items, reinterpret_cast<uint32_t*>(w + L.l_counts),
+      reinterpret_cast<uint32_t*>(w + L.l_errs), reinterpret_cast<uint32_t*>(w + L.l_sizes),
+      w + L.scratch, s, d);
+  if (e != cudaSuccess) return PSS_ERR_CUDA;
+  return tree_and_verify(d_A, n, kb, k, P, d_out_items, d_out_counts, d_out_len, w, L, s, d);
+}
+
+// chunks of the pipelined host->device copy in pss_query_host (1 = copy, then compute)
+static uint32_t h2d_chunks(uint64_t n, int kb, uint32_t P) {
+  uint64_t G = n * kb >= (64ull << 20) ? 16 : 1;
+  if (const char* v = std::getenv("PSS_DEBUG_H2D_CHUNKS")) G = (uint64_t)std::atoll(v);
+  G = std::min<uint64_t>({G, (uint64_t)P, (uint64_t)SS_MAX_RANGES});
+  return G ? (uint32_t)G : 1u;
 }
 
 pss_status pss_query(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k, uint32_t P,
@@ -222,12 +243,52 @@ pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type k
   if (ws_bytes < L.total) return PSS_ERR_WORKSPACE_TOO_SMALL;
   unsigned char* w = static_cast<unsigned char*>(d_ws);
   cudaError_t e = cudaSuccess;
-  if (n) e = cudaMemcpyAsync(d_A, h_A, n * kb, cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) return PSS_ERR_CUDA;
-  pss_status st = query_impl(d_A, n, kb, k, P, w + L.o_items,
-                             reinterpret_cast<uint64_t*>(w + L.o_counts),
-                             reinterpret_cast<uint32_t*>(w + L.o_len), w, L, stream, d);
-  if (st != PSS_OK) return st;
+  // The copy of A is cut at partition boundaries into G chunks on a private copy stream; the
+  // leaves of chunk g are summarized on `stream` as soon as its bytes have landed, so the
+  // summaries overlap the host->device transfer and only the last chunk's leaves, the merge
+  // tree and the verification pass (which needs all of A) run after it.
+  const uint32_t G = h2d_chunks(n, kb, P);
+  if (G <= 1) {
+    if (n) e = cudaMemcpyAsync(d_A, h_A, n * kb, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return PSS_ERR_CUDA;
+    pss_status st = query_impl(d_A, n, kb, k, P, w + L.o_items,
+                               reinterpret_cast<uint64_t*>(w + L.o_counts),
+                               reinterpret_cast<uint32_t*>(w + L.o_len), w, L, stream, d);
+    if (st != PSS_OK) return st;
+  } else {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[SS_MAX_RANGES + 1] = {};
+    e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (uint32_t g = 0; g <= G && e == cudaSuccess; ++g)
+      e = cudaEventCreateWithFlags(&ev[g], cudaEventDisableTiming);
+    // the copies must not overwrite d_A before earlier work on `stream` is done with it
+    if (e == cudaSuccess) e = cudaEventRecord(ev[G], stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[G], 0);
+    const char* hA = static_cast<const char*>(h_A);
+    char* dA = static_cast<char*>(d_A);
+    for (uint32_t g = 0; g < G && e == cudaSuccess; ++g) {
+      const uint32_t r0 = (uint32_t)((uint64_t)g * P / G), r1 = (uint32_t)((uint64_t)(g + 1) * P / G);
+      const uint64_t lo = (uint64_t)r0 * n / P, hi = (uint64_t)r1 * n / P;  // a1 bounds
+      e = cudaMemcpyAsync(dA + lo * kb, hA + lo * kb, (hi - lo) * kb, cudaMemcpyHostToDevice, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[g], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ev[g], 0);
+      if (e == cudaSuccess)
+        e = summarize_launch(d_A, n, kb, k, P, w + L.l_items,
+                             reinterpret_cast<uint32_t*>(w + L.l_counts),
+                             reinterpret_cast<uint32_t*>(w + L.l_errs),
+                             reinterpret_cast<uint32_t*>(w + L.l_sizes), w + L.scratch, stream, d,
+                             r0, r1, g);
+    }
+    // stream-ordered release: destruction waits for the enqueued work
+    for (uint32_t g = 0; g <= G; ++g)
+      if (ev[g]) cudaEventDestroy(ev[g]);
+    if (cs) cudaStreamDestroy(cs);
+    if (e != cudaSuccess) return PSS_ERR_CUDA;
+    pss_status st = tree_and_verify(d_A, n, kb, k, P, w + L.o_items,
+                                    reinterpret_cast<uint64_t*>(w + L.o_counts),
+                                    reinterpret_cast<uint32_t*>(w + L.o_len), w, L, stream, d);
+    if (st != PSS_OK) return st;
+  }
   e = cudaMemcpyAsync(h_out_len, w + L.o_len, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(h_out_items, w + L.o_items, (size_t)k * kb, cudaMemcpyDeviceToHost, stream);

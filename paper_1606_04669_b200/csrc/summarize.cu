@@ -162,6 +162,7 @@ struct SumArgs {
   const void* A;
   uint64_t n;
   uint32_t k, P;
+  uint32_t r0, r1;  // this launch summarizes partitions [r0, r1) of the P-way decomposition
   void* items;
   uint32_t* counts;
   uint32_t* errs;
@@ -218,9 +219,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 
   while (true) {
     uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(a.queue, 1u);
+    if (lane == 0) r = a.r0 + atomicAdd(a.queue, 1u);
     r = __shfl_sync(PSS_FULL, r, 0);
-    if (r >= P) break;
+    if (r >= a.r1) break;
     const uint64_t lo = (uint64_t)r * n / P;  // Alg. 1 l.3-4: r*n < 2^63 as n <= 2^31
     const uint64_t hi = (uint64_t)(r + 1) * n / P;
     const uint32_t L = (uint32_t)(hi - lo);
@@ -471,11 +472,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
         const KT x = ring[(roff + q + lane) % RING];
-#ifdef PSS_EXP_MATCH2  // timing experiment only (tools/variant.sh): a second, redundant match
-        const uint32_t grp = __match_any_sync(PSS_FULL, x) & __match_any_sync(PSS_FULL, x + 1) & amask;
-#else
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
-#endif
         SS_TICK(ph1, tk, grp);
 
         // victims for this step (independent of the lookups): lane j holds the j-th next slot
@@ -598,7 +595,8 @@ struct SSPlan {
   uint32_t cb, sb, fmask;
   SSLayout L;
   size_t smem;
-  int grid;
+  int grid;   // CTAs of a launch over all P partitions
+  int slots;  // resident CTAs the device holds
 };
 
 template <typename KT, typename ET, bool G, bool PK>
@@ -637,6 +635,7 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
       nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(p.smem)
                    : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(p.smem);
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)nb * d.sms);
+    p.slots = (int)std::min<uint64_t>((uint64_t)nb * d.sms, 1u << 30);
   } else {
     p.packed = false;
     p.sb = 32;
@@ -644,6 +643,7 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     p.L = ss_layout(k, kb, 8, false);
     p.smem = SS_RING_BYTES + 64;
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
+    p.slots = 8 * d.sms;
   }
   if (p.grid < 1) p.grid = 1;
   return p;
@@ -652,28 +652,34 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
 size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
   SSPlan p = ss_plan(n, kb, k, P, d);
   Bump b;
-  b.take<uint32_t>(1);
+  b.take<uint32_t>(SS_MAX_RANGES);
   if (p.gstate) b.take<unsigned char>(p.L.total * (size_t)p.grid);
   return b.bytes();
 }
 
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
-                             void* ws, cudaStream_t s, const DevInfo& d) {
+                             void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0,
+                             uint32_t r1, uint32_t qi) {
   SSPlan p = ss_plan(n, kb, k, P, d);
+  if (r1 > P) r1 = P;
+  if (r0 >= r1 || qi >= SS_MAX_RANGES) return cudaErrorInvalidValue;
+  const int grid = (int)std::min<uint64_t>(r1 - r0, (uint64_t)p.grid);
   Bump b;
-  const size_t oq = b.take<uint32_t>(1);
+  const size_t oq = b.take<uint32_t>(SS_MAX_RANGES);
   const size_t og = p.gstate ? b.take<unsigned char>(p.L.total * (size_t)p.grid) : 0;
   SumArgs a;
   a.A = A;
   a.n = n;
   a.k = k;
   a.P = P;
+  a.r0 = r0;
+  a.r1 = r1;
   a.items = items;
   a.counts = counts;
   a.errs = errs;
   a.sizes = sizes;
-  a.queue = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ws) + oq);
+  a.queue = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ws) + oq) + qi;
   a.gstate = p.gstate ? static_cast<unsigned char*>(ws) + og : nullptr;
   a.gstride = p.L.total;
   a.o_cnt = p.L.cnt;
@@ -691,20 +697,20 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   if (!p.gstate) {
     if (p.packed) {
       if (kb == 4)
-        ss_summarize_kernel<uint32_t, uint16_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint32_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
       else
-        ss_summarize_kernel<uint64_t, uint16_t, false, true><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint64_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
     } else {
       if (kb == 4)
-        ss_summarize_kernel<uint32_t, uint16_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint32_t, uint16_t, false, false><<<grid, 32, p.smem, s>>>(a);
       else
-        ss_summarize_kernel<uint64_t, uint16_t, false, false><<<p.grid, 32, p.smem, s>>>(a);
+        ss_summarize_kernel<uint64_t, uint16_t, false, false><<<grid, 32, p.smem, s>>>(a);
     }
   } else {
     if (kb == 4)
-      ss_summarize_kernel<uint32_t, uint64_t, true, false><<<p.grid, 32, p.smem, s>>>(a);
+      ss_summarize_kernel<uint32_t, uint64_t, true, false><<<grid, 32, p.smem, s>>>(a);
     else
-      ss_summarize_kernel<uint64_t, uint64_t, true, false><<<p.grid, 32, p.smem, s>>>(a);
+      ss_summarize_kernel<uint64_t, uint64_t, true, false><<<grid, 32, p.smem, s>>>(a);
   }
   return cudaGetLastError();
 }

@@ -226,6 +226,19 @@ def test_query_host_end_to_end(pss):
     assert counts.numpy().tolist() == ref.result[1].tolist()
 
 
+@pytest.mark.parametrize("chunks,kb,k,P", [(3, 4, 200, 16), (16, 4, 100, 37), (7, 8, 64, 29),
+                                           (5, 4, 4500, 11), (64, 4, 50, 64)])
+def test_query_host_pipelined_copy(pss, monkeypatch, chunks, kb, k, P):
+    """pss_query_host cut into copy chunks at partition boundaries (each chunk's leaves are
+    summarized while later chunks are in flight): same answer as the oracle, ragged n and P."""
+    monkeypatch.setenv("PSS_DEBUG_H2D_CHUNKS", str(chunks))
+    A = inputs.zipf((1 << 19) + 12345, 1.2, 1e6, seed=31 + chunks, key_bytes=kb)
+    items, counts = pss.pss_query_host(torch.from_numpy(A).pin_memory(), k, P)
+    ref = oracle.pipeline(A, k, P, threads=8)
+    assert items.numpy().astype(np.uint64).tolist() == ref.result[0].tolist()
+    assert counts.numpy().tolist() == ref.result[1].tolist()
+
+
 # ---------------------------------------------------------------- full BASELINE sizes
 def bruteforce_kmajority(A, k):
     u, c = np.unique(A, return_counts=True)
