@@ -19,10 +19,19 @@
 
 namespace pss {
 
-constexpr int VTHREADS = 128;
+#ifndef PSS_VT_THREADS
+#define PSS_VT_THREADS 128
+#endif
+#ifndef PSS_VT_EXP
+#define PSS_VT_EXP 0
+#endif
+#ifndef PSS_VT_U
+#define PSS_VT_U 4
+#endif
+constexpr int VTHREADS = PSS_VT_THREADS;
 constexpr int VWARPS = VTHREADS / 32;
 constexpr uint32_t VT_SMEM = 2048;       // table entries staged in shared memory
-constexpr uint32_t VC_BYTES = 32 * 1024; // shared-memory counter area per CTA
+constexpr uint32_t VC_BYTES = VWARPS * 8192;  // shared-memory counter area per CTA
 constexpr uint32_t VLANE_MAX = VC_BYTES / (VWARPS * 32 * 2);  // nc for per-lane 16-bit counters
 constexpr uint32_t VWARP_MAX = VC_BYTES / (VWARPS * 4);       // nc for per-warp 32-bit counters
 
@@ -200,6 +209,109 @@ __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t
   }
 }
 
+// fire-and-forget shared-memory add (no return value, so no scoreboard wait on the result)
+__device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// One warp's scan of its share of A. MODE 0: per-lane 16-bit counters, two per 32-bit word laid
+// out [cand / 2][lane] (a warp's adds hit 32 banks and never the same word), added with
+// red.shared so successive increments do not wait on each other; MODE 1: __match_any_sync groups
+// + per-warp 32-bit counters; MODE 2: groups + 64-bit global atomics. PERF: one-probe table.
+template <typename KT, int MODE, bool PERF>
+__device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n,
+                                            const typename VEnt<KT>::T* tab, uint32_t seed,
+                                            uint32_t logT, uint32_t* lw, uint32_t* wc,
+                                            unsigned long long* acc, uint64_t wid,
+                                            uint64_t nwarps) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t ltm = lanemask_lt();
+#if PSS_VT_EXP == 2 || PSS_VT_EXP == 3  // timing experiment: no table lookup
+  auto look = [&](KT x) { return (uint32_t)x & 31u; };
+#else
+  auto look = [&](KT x) { return vlookup<KT>(tab, x, seed, logT, PERF); };
+#endif
+#if PSS_VT_EXP == 1 || PSS_VT_EXP == 3  // timing experiment: no counting
+  uint32_t sink = 0;
+  auto count1 = [&](uint32_t j) { sink += j; };
+#else
+  auto count1 = [&](uint32_t j) {
+    if (MODE == 0) {
+      if (j != 0xffffffffu) red_shared_add(lw + (j >> 1) * 32 + lane, 1u << ((j & 1u) << 4));
+    } else {
+      const uint32_t g = __match_any_sync(PSS_FULL, j);
+      if ((g & ltm) == 0 && j != 0xffffffffu) {
+        if (MODE == 1)
+          wc[j] += __popc(g);
+        else
+          atomicAdd(&acc[j], (unsigned long long)__popc(g));
+      }
+    }
+  };
+#endif
+
+  constexpr uint32_t E = 16 / sizeof(KT);
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(A);
+  uint64_t head = ((16u - (addr & 15u)) & 15u) / sizeof(KT);
+  if ((addr % sizeof(KT)) != 0) head = n;  // not naturally aligned: scalar path only
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / E;
+  const uint64_t tail0 = head + nvec * E;
+  // scalar head and tail (warp-uniform loops)
+  for (uint64_t base = wid * 32; base < head; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    count1(i < head ? look(A[i]) : 0xffffffffu);
+  }
+  const uint4* V = reinterpret_cast<const uint4*>(A + head);
+  const uint64_t stride = nwarps * 32;
+  // software pipeline over U 16-byte loads per lane; all lanes of a warp take the same trip count
+  constexpr int U = PSS_VT_U;
+  uint4 q[U], nq[U];
+  uint64_t vb = wid * 32;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t va = vb + u * stride + lane;
+    q[u] = va < nvec ? __ldg(V + va) : make_uint4(0, 0, 0, 0);
+  }
+  // steady state: this batch and the next one lie entirely inside A, no bounds checks
+  for (; vb + 2 * U * stride <= nvec; vb += U * stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) nq[u] = __ldg(V + vb + (U + u) * stride + lane);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const KT* xs = reinterpret_cast<const KT*>(&q[u]);
+#pragma unroll
+      for (uint32_t e = 0; e < E; ++e) count1(look(xs[e]));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = nq[u];
+  }
+  for (; vb < nvec; vb += U * stride) {
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ok[u] = vb + u * stride + lane < nvec;
+      const uint64_t vn = vb + (U + u) * stride + lane;
+      nq[u] = vn < nvec ? __ldg(V + vn) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const KT* xs = reinterpret_cast<const KT*>(&q[u]);
+#pragma unroll
+      for (uint32_t e = 0; e < E; ++e) count1(ok[u] ? look(xs[e]) : 0xffffffffu);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = nq[u];
+  }
+  for (uint64_t base = tail0 + wid * 32; base < n; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    count1(i < n ? look(A[i]) : 0xffffffffu);
+  }
+#if PSS_VT_EXP == 1 || PSS_VT_EXP == 3
+  if (sink == 0x12345678u) acc[0] = sink;
+#endif
+}
+
 // lane_ok: per-lane 16-bit counters cannot overflow for this launch (host-checked)
 template <typename KT>
 __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__ A, uint64_t n,
@@ -214,103 +326,48 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint32_t seed = ctl[0], logT = ctl[1];
   const bool perf = ctl[2] != 0;
   const uint32_t T = 1u << logT;
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
-  const int mode = (lane_ok && nc <= VLANE_MAX) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
+  const int mode = (lane_ok && nc <= VLANE_MAX && T <= VT_SMEM) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
   VT* stab = reinterpret_cast<VT*>(vsm);
   unsigned char* carea = vsm + (size_t)VT_SMEM * sizeof(VT);
-  uint16_t* lc = reinterpret_cast<uint16_t*>(carea) + (size_t)warp * nc * 32;  // [cand][lane]
-  uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;       // [cand]
+  const uint32_t ncw = (nc + 1) / 2;  // words per lane in mode 0
+  uint32_t* lw = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * ncw * 32;  // [cand/2][lane]
+  uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;        // [cand]
   const bool tab_smem = T <= VT_SMEM;
   if (tab_smem)
     for (uint32_t h = threadIdx.x; h < T; h += VTHREADS) stab[h] = gtab[h];
   if (mode == 0)
-    for (uint32_t i = threadIdx.x; i < VWARPS * nc * 32; i += VTHREADS)
-      reinterpret_cast<uint16_t*>(carea)[i] = 0;
+    for (uint32_t i = threadIdx.x; i < VWARPS * ncw * 32; i += VTHREADS)
+      reinterpret_cast<uint32_t*>(carea)[i] = 0;
   else if (mode == 1)
     for (uint32_t i = threadIdx.x; i < VWARPS * nc; i += VTHREADS)
       reinterpret_cast<uint32_t*>(carea)[i] = 0;
   __syncthreads();
-  const VT* tab = tab_smem ? stab : gtab;
-
-  // count the candidate indices j[0..NJ) of one step of the warp
-  auto count = [&](const uint32_t* j, int NJ) {
-    if (mode == 0) {
-      for (int t = 0; t < NJ; ++t)
-        if (j[t] != 0xffffffffu) lc[j[t] * 32 + lane] += 1;
-    } else {
-      const uint32_t ltm = lanemask_lt();
-      for (int t = 0; t < NJ; ++t) {
-        const uint32_t g = __match_any_sync(PSS_FULL, j[t]);
-        if ((g & ltm) == 0 && j[t] != 0xffffffffu) {
-          if (mode == 1)
-            wc[j[t]] += __popc(g);
-          else
-            atomicAdd(&acc[j[t]], (unsigned long long)__popc(g));
-        }
-      }
-    }
-  };
-
-  constexpr uint32_t E = 16 / sizeof(KT);
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(A);
-  uint64_t head = ((16u - (addr & 15u)) & 15u) / sizeof(KT);
-  if ((addr % sizeof(KT)) != 0) head = n;  // not naturally aligned: scalar path only
-  if (head > n) head = n;
-  const uint64_t nvec = (n - head) / E;
-  const uint64_t tail0 = head + nvec * E;
   const uint64_t wid = (uint64_t)blockIdx.x * VWARPS + warp;
   const uint64_t nwarps = (uint64_t)gridDim.x * VWARPS;
-  // scalar head and tail (warp-uniform loops)
-  for (uint64_t base = wid * 32; base < head; base += nwarps * 32) {
-    const uint64_t i = base + lane;
-    uint32_t j = i < head ? vlookup<KT>(tab, A[i], seed, logT, perf) : 0xffffffffu;
-    count(&j, 1);
-  }
-  const uint4* V = reinterpret_cast<const uint4*>(A + head);
-  const uint64_t stride = nwarps * 32;
-  // software pipeline over U 16-byte loads per lane; all lanes of a warp take the same trip count
-  constexpr int U = 4;
-  uint4 q[U], nq[U];
-  uint64_t vb = wid * 32;
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint64_t va = vb + u * stride + lane;
-    q[u] = va < nvec ? __ldg(V + va) : make_uint4(0, 0, 0, 0);
-  }
-  for (; vb < nvec; vb += U * stride) {
-    bool ok[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      ok[u] = vb + u * stride + lane < nvec;
-      const uint64_t vn = vb + (U + u) * stride + lane;
-      nq[u] = vn < nvec ? __ldg(V + vn) : make_uint4(0, 0, 0, 0);
-    }
-    uint32_t j[U * E];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const KT* xs = reinterpret_cast<const KT*>(&q[u]);
-#pragma unroll
-      for (uint32_t e = 0; e < E; ++e)
-        j[u * E + e] = ok[u] ? vlookup<KT>(tab, xs[e], seed, logT, perf) : 0xffffffffu;
-    }
-    count(j, U * E);
-#pragma unroll
-    for (int u = 0; u < U; ++u) q[u] = nq[u];
-  }
-  for (uint64_t base = tail0 + wid * 32; base < n; base += nwarps * 32) {
-    const uint64_t i = base + lane;
-    uint32_t j = i < n ? vlookup<KT>(tab, A[i], seed, logT, perf) : 0xffffffffu;
-    count(&j, 1);
+  if (mode == 0) {
+    if (perf)
+      verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps);
+    else
+      verify_scan<KT, 0, false>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps);
+  } else {
+    const VT* tab = tab_smem ? stab : gtab;
+    if (mode == 1)
+      verify_scan<KT, 1, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps);
+    else
+      verify_scan<KT, 2, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps);
   }
   if (mode != 2) {
     __syncthreads();
     for (uint32_t c = threadIdx.x; c < nc; c += VTHREADS) {
       unsigned long long t = 0;
       if (mode == 0) {
-        const uint16_t* base = reinterpret_cast<const uint16_t*>(carea);
+        const uint32_t* base = reinterpret_cast<const uint32_t*>(carea);
+        const uint32_t sh = (c & 1u) << 4;
         for (uint32_t w = 0; w < VWARPS; ++w)
-          for (uint32_t l = 0; l < 32; ++l) t += base[((size_t)w * nc + c) * 32 + l];
+          for (uint32_t l = 0; l < 32; ++l)
+            t += (base[((size_t)w * ncw + (c >> 1)) * 32 + l] >> sh) & 0xffffu;
       } else {
         const uint32_t* base = reinterpret_cast<const uint32_t*>(carea);
         for (uint32_t w = 0; w < VWARPS; ++w) t += base[(size_t)w * nc + c];
