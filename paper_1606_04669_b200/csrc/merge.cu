@@ -66,6 +66,30 @@ static MLayout m_layout(uint32_t k, int kb, uint32_t NP) {
   return L;
 }
 
+#ifdef PSS_MSTATS  // debug build only (tools/merge_stats.py): per-phase SM cycles of a COMBINE
+__device__ unsigned long long g_m_stats[16][16];  // [ceil_log2(nblocks)][phase]
+}  // namespace pss
+extern "C" int pss_debug_mstats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pss::g_m_stats, sizeof(pss::g_m_stats));
+  if (reset) {
+    static unsigned long long z[16][16] = {};
+    cudaMemcpyToSymbol(pss::g_m_stats, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+namespace pss {
+__device__ __forceinline__ void m_tick(int ph, uint32_t lv) {
+  __shared__ long long prev;
+  if (threadIdx.x == 0) {
+    const long long t = clock64();
+    if (ph >= 0) atomicAdd(&g_m_stats[lv & 15][ph], (unsigned long long)(t - prev));
+    prev = t;
+  }
+}
+#else
+__device__ __forceinline__ void m_tick(int, uint32_t) {}
+#endif
+
 template <int NT>
 __device__ __forceinline__ uint32_t block_reduce(uint32_t v, uint32_t* red, bool is_min) {
   v = is_min ? __reduce_min_sync(PSS_FULL, v) : __reduce_add_sync(PSS_FULL, v);
@@ -227,75 +251,152 @@ __device__ __forceinline__ void radix_pick(uint32_t* hist, uint32_t need, bool f
   }
 }
 
+// counters tied at the threshold count ranked by brute force (each against all) up to this many
+constexpr uint32_t TIE_RANK_MAX = 128;
+
+// warp-aggregated append: lanes with `take` get consecutive positions from *ctr (one atomic per
+// warp); returns this lane's position (undefined if !take). All lanes of the warp must call it.
+__device__ __forceinline__ uint32_t warp_append(uint32_t* ctr, bool take) {
+  const uint32_t b = __ballot_sync(PSS_FULL, take);
+  if (!b) return 0;
+  const uint32_t lead = (uint32_t)(__ffs(b) - 1);
+  uint32_t off = 0;
+  if ((threadIdx.x & 31u) == lead) off = atomicAdd(ctr, (uint32_t)__popc(b));
+  off = __shfl_sync(PSS_FULL, off, lead);
+  return off + (uint32_t)__popc(b & lanemask_lt());
+}
+
 // Prune(k) for an internal tree node: the k greatest counters by (count desc, item asc) as a
-// set, in no particular order (COMBINE does not depend on the order of its inputs). Radix select
-// of the threshold count C, then of the threshold item among the counters with count C.
+// set, in no particular order (COMBINE does not depend on the order of its inputs).
+//   1. live count and live min/max count (one block reduction);
+//   2. threshold count C by radix select on 8-bit digits, from the highest digit in which the
+//      live minimum and maximum differ (the digits above are common to all counters);
+//   3. the counters with count == C are compacted into a list (tl = union index, tkey = item);
+//      if more of them are tied than still needed, the threshold item K is the need-th smallest
+//      item of the list: by brute-force ranking for short lists, else by radix select on it;
+//   4. the selected counters are appended to the output (warp-aggregated positions).
 template <typename KT, int NT>
 __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT* ukey,
                                   const uint32_t* ucnt, const uint32_t* uerr, const uint8_t* dead,
-                                  uint32_t* hist, uint32_t* red, KT* oi, uint32_t* oc,
-                                  uint32_t* oe, uint32_t* osize) {
-  const uint32_t tid = threadIdx.x;
-  uint32_t live = 0;
-  for (uint32_t i = tid; i < N; i += NT) live += !(i >= n1 && dead[i - n1]);
-  const uint32_t Lv = block_reduce<NT>(live, red, false);
+                                  uint32_t* hist, uint32_t* red, uint32_t* tl, KT* tkey, KT* oi,
+                                  uint32_t* oc, uint32_t* oe, uint32_t* osize, uint32_t lv) {
+  constexpr int NW = NT / 32;
+  __shared__ KT kres;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  uint32_t live = 0, mn = 0xffffffffu, mx = 0;
+  for (uint32_t i = tid; i < N; i += NT) {
+    if (i >= n1 && dead[i - n1]) continue;
+    const uint32_t c = ucnt[i];
+    ++live;
+    mn = min(mn, c);
+    mx = max(mx, c);
+  }
+  live = __reduce_add_sync(PSS_FULL, live);
+  mn = __reduce_min_sync(PSS_FULL, mn);
+  mx = __reduce_max_sync(PSS_FULL, mx);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = live;
+    red[NW + warp] = mn;
+    red[2 * NW + warp] = mx;
+  }
+  if (tid == 0) {
+    hist[258] = 0;
+    hist[259] = 0;
+  }
+  __syncthreads();
+  uint32_t Lv = 0;
+  mn = 0xffffffffu;
+  mx = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    Lv += red[w];
+    mn = min(mn, red[NW + w]);
+    mx = max(mx, red[2 * NW + w]);
+  }
+  m_tick(5, lv);
   const bool all = Lv <= k;
   uint32_t need = k;
   uint32_t C = 0;       // threshold count
   KT K = (KT)0;         // threshold item among count == C (inclusive)
   bool all_eq = true;   // take every counter with count == C
   if (!all) {
-    uint32_t mask = 0;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
-      __syncthreads();
-      for (uint32_t i = tid; i < N; i += NT) {
-        if (i >= n1 && dead[i - n1]) continue;
-        const uint32_t c = ucnt[i];
-        if ((c & mask) == C) atomicAdd(&hist[(c >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (tid < 32) radix_pick(hist, need, true);
-      __syncthreads();
-      need -= hist[257];
-      C |= hist[256] << shift;
-      mask |= 255u << shift;
-      __syncthreads();
-    }
-    // counters with count == C: `need` of them, the smallest items
-    uint32_t eq = 0;
-    for (uint32_t i = tid; i < N; i += NT)
-      eq += !(i >= n1 && dead[i - n1]) && ucnt[i] == C;
-    eq = block_reduce<NT>(eq, red, false);
-    all_eq = eq == need;
-    if (!all_eq) {
-      KT kmask = 0;
-      for (int shift = 8 * (int)sizeof(KT) - 8; shift >= 0; shift -= 8) {
+    if (mn == mx) {
+      C = mn;
+    } else {
+      const int top = 31 - __clz(mn ^ mx);
+      int shift = top / 8 * 8;
+      uint32_t mask = shift >= 24 ? 0u : ~((1u << (shift + 8)) - 1u);
+      C = mn & mask;
+      for (; shift >= 0; shift -= 8) {
         for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
         __syncthreads();
         for (uint32_t i = tid; i < N; i += NT) {
           if (i >= n1 && dead[i - n1]) continue;
-          const KT x = ukey[i];
-          if (ucnt[i] == C && (x & kmask) == K) atomicAdd(&hist[(uint32_t)(x >> shift) & 255u], 1u);
+          const uint32_t c = ucnt[i];
+          if ((c & mask) == C) atomicAdd(&hist[(c >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (tid < 32) radix_pick(hist, need, false);
+        if (tid < 32) radix_pick(hist, need, true);
         __syncthreads();
         need -= hist[257];
-        K |= (KT)hist[256] << shift;
-        kmask |= (KT)255 << shift;
+        C |= hist[256] << shift;
+        mask |= 255u << shift;
         __syncthreads();
       }
     }
+    m_tick(6, lv);
+    // the counters with count == C, `need` of which are taken (the smallest items)
+    for (uint32_t base = warp * 32; base < N; base += NT) {
+      const uint32_t i = base + lane;
+      const bool t = i < N && !(i >= n1 && dead[i - n1]) && ucnt[i] == C;
+      const uint32_t o = warp_append(&hist[259], t);
+      if (t) {
+        tl[o] = i;
+        tkey[o] = ukey[i];
+      }
+    }
+    __syncthreads();
+    const uint32_t E = hist[259];
+    all_eq = E == need;
+    if (!all_eq) {
+      if (E <= TIE_RANK_MAX) {  // items in the union are distinct: ranks are exact
+        for (uint32_t j = tid; j < E; j += NT) {
+          const KT x = tkey[j];
+          uint32_t r = 0;
+          for (uint32_t u = 0; u < E; ++u) r += tkey[u] < x;
+          if (r == need - 1) kres = x;
+        }
+        __syncthreads();
+        K = kres;
+      } else {
+        KT kmask = 0;
+        for (int shift = 8 * (int)sizeof(KT) - 8; shift >= 0; shift -= 8) {
+          for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
+          __syncthreads();
+          for (uint32_t j = tid; j < E; j += NT) {
+            const KT x = tkey[j];
+            if ((x & kmask) == K) atomicAdd(&hist[(uint32_t)(x >> shift) & 255u], 1u);
+          }
+          __syncthreads();
+          if (tid < 32) radix_pick(hist, need, false);
+          __syncthreads();
+          need -= hist[257];
+          K |= (KT)hist[256] << shift;
+          kmask |= (KT)255 << shift;
+          __syncthreads();
+        }
+      }
+    }
   }
-  if (tid == 0) hist[258] = 0;
-  __syncthreads();
-  for (uint32_t i = tid; i < N; i += NT) {
-    if (i >= n1 && dead[i - n1]) continue;
-    const uint32_t c = ucnt[i];
-    const bool tk = all || c > C || (c == C && (all_eq || ukey[i] <= K));
+  m_tick(7, lv);
+  for (uint32_t base = warp * 32; base < N; base += NT) {
+    const uint32_t i = base + lane;
+    const bool lvv = i < N && !(i >= n1 && dead[i - n1]);
+    const uint32_t c = lvv ? ucnt[i] : 0u;
+    const bool tk = lvv && (all || c > C || (c == C && (all_eq || ukey[i] <= K)));
+    const uint32_t o = warp_append(&hist[258], tk);
     if (tk) {
-      const uint32_t o = atomicAdd(&hist[258], 1u);
       oi[o] = ukey[i];
       oc[o] = c;
       oe[o] = uerr[i];
@@ -303,13 +404,14 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
   }
   __syncthreads();
   if (tid == 0) *osize = hist[258];
+  m_tick(8, lv);
 }
 
 // EPT > 0: the sort keeps EPT elements per thread in registers; EPT == 0: shared-memory sort
 template <typename KT, bool G, int NT, int EPT>
 __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint32_t red[NT / 32];
+  __shared__ uint32_t red[3 * (NT / 32)];
   __shared__ uint32_t hist[260];
   const uint32_t NP = a.NP;
   const uint32_t k = a.k;
@@ -325,7 +427,9 @@ __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
   KT* xlo = reinterpret_cast<KT*>(xidx + NP);
   const uint32_t H2 = 1u << a.logH2, hmask = H2 - 1u;
 
+  const uint32_t lv = ceil_log2(a.nblocks);
   for (uint32_t blk = blockIdx.x; blk < a.nblocks; blk += gridDim.x) {
+    m_tick(-1, lv);
     const uint32_t li = blk * a.a_mul + a.a_add;
     const bool has_r = blk < a.nright;
     const uint32_t ri = blk * a.b_mul + a.b_add;
@@ -351,34 +455,62 @@ __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
     const uint32_t* c2 = has_r ? a.b.counts + (size_t)ri * k : nullptr;
     const uint32_t* e2 = has_r ? a.b.errs + (size_t)ri * k : nullptr;
 
-    // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4)
+    // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4). The loads of
+    // both summaries are issued before their stores.
     uint32_t mn1 = 0xffffffffu, mn2 = 0xffffffffu;
-    for (uint32_t t = tid; t < n1; t += NT) {
-      ukey[t] = i1[t];
-      const uint32_t c = c1[t];
-      ucnt[t] = c;
-      uerr[t] = e1[t];
-      mn1 = min(mn1, c);
-    }
-    for (uint32_t t = tid; t < n2; t += NT) {
-      ukey[n1 + t] = i2[t];
-      const uint32_t c = c2[t];
-      ucnt[n1 + t] = c;
-      uerr[n1 + t] = e2[t];
-      dead[t] = 0;
-      mn2 = min(mn2, c);
+    for (uint32_t t = tid; t < max(n1, n2); t += NT) {
+      const bool h1 = t < n1, h2 = t < n2;
+      KT x1 = 0, x2 = 0;
+      uint32_t cc1 = 0, ee1 = 0, cc2 = 0, ee2 = 0;
+      if (h1) {
+        x1 = __ldg(i1 + t);
+        cc1 = __ldg(c1 + t);
+        ee1 = __ldg(e1 + t);
+      }
+      if (h2) {
+        x2 = __ldg(i2 + t);
+        cc2 = __ldg(c2 + t);
+        ee2 = __ldg(e2 + t);
+      }
+      if (h1) {
+        ukey[t] = x1;
+        ucnt[t] = cc1;
+        uerr[t] = ee1;
+        mn1 = min(mn1, cc1);
+      }
+      if (h2) {
+        ukey[n1 + t] = x2;
+        ucnt[n1 + t] = cc2;
+        uerr[n1 + t] = ee2;
+        dead[t] = 0;
+        mn2 = min(mn2, cc2);
+      }
     }
     for (uint32_t h = tid; h < H2; h += NT) ht[h] = 0xffffffffu;
-    const uint32_t m1r = block_reduce<NT>(mn1, red, true);
-    const uint32_t m2r = block_reduce<NT>(mn2, red, true);
+    mn1 = __reduce_min_sync(PSS_FULL, mn1);
+    mn2 = __reduce_min_sync(PSS_FULL, mn2);
+    __syncthreads();
+    if ((tid & 31u) == 0) {
+      red[tid >> 5] = mn1;
+      red[NT / 32 + (tid >> 5)] = mn2;
+    }
+    __syncthreads();
+    uint32_t m1r = 0xffffffffu, m2r = 0xffffffffu;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+      m1r = min(m1r, red[w]);
+      m2r = min(m2r, red[NT / 32 + w]);
+    }
     const uint32_t m1 = n1 == k ? m1r : 0u;
     const uint32_t m2 = n2 == k ? m2r : 0u;
+    m_tick(0, lv);
     // index S2's items (Find of Alg. 2 l.5)
     for (uint32_t t = tid; t < n2; t += NT) {
       uint32_t h = hslot(ukey[n1 + t], a.logH2);
       while (atomicCAS(&ht[h], 0xffffffffu, t) != 0xffffffffu) h = (h + 1u) & hmask;
     }
     __syncthreads();
+    m_tick(1, lv);
     // counters of S1: matched -> f1 + f2 and Remove from S2; else f1 + m2 (Alg. 2 l.4-13)
     for (uint32_t t = tid; t < n1; t += NT) {
       const KT x = ukey[t];
@@ -395,6 +527,7 @@ __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
       }
     }
     __syncthreads();
+    m_tick(2, lv);
     // remaining counters of S2: f2 + m1 (Alg. 2 l.14-18)
     for (uint32_t t = tid; t < n2; t += NT)
       if (!dead[t]) {
@@ -402,11 +535,17 @@ __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
         uerr[n1 + t] += m1;
       }
     __syncthreads();
+    m_tick(3, lv);
     // Prune(k) (Alg. 2 l.19): order by (count desc, item asc), keep the first k (R5)
     const uint32_t N = n1 + n2;
     if (!a.sort_out) {  // internal tree node: the top-k set
-      select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, oi, oc, oe,
-                                a.o.sizes + blk);
+      select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, xidx, xlo, oi, oc,
+                                oe, a.o.sizes + blk, lv);
+      if (tid == 0) {
+#ifdef PSS_MSTATS
+        atomicAdd(&g_m_stats[lv & 15][15], 1ull);
+#endif
+      }
       continue;
     }
     if constexpr (EPT > 0) {
