@@ -485,8 +485,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
         const KT x = ring[(roff + q + lane) % RING];
-        const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
-        SS_TICK(ph1, tk, grp);
+        // the match is issued first and its result first used after the lookups, so that its
+        // latency (it grows with the number of distinct keys) overlaps them
+        const uint32_t grp_all = __match_any_sync(PSS_FULL, x);
 
         // victims for this step (independent of the lookups): lane j holds the j-th next slot
         // of B_m at or after the cursor (two bitmap words) and the index entry of its item
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         uint32_t ce, fi, fp;
         lookup(x, act, s, ce, fi, fp);
         SS_TICK(ph2, tk, ce ^ (uint32_t)s ^ myop);
+        const uint32_t grp = grp_all & amask;
         const bool hit = s >= 0;
         const uint32_t cs = ce & CM;
         const bool leader = act && (grp & ltm) == 0;
