@@ -69,11 +69,15 @@ namespace pss {
 
 // per-warp TMA ring: 3 stages of 512 bytes (a step spans at most two stages; one more in flight)
 constexpr uint32_t SS_NSTAGE = 3;
-constexpr uint32_t SS_STAGE_BYTES = 512;
+#ifndef PSS_SS_STAGE_BYTES
+#define PSS_SS_STAGE_BYTES 512
+#endif
+constexpr uint32_t SS_STAGE_BYTES = PSS_SS_STAGE_BYTES;
+constexpr uint32_t SS_BAR_BYTES = 32;  // the ring's mbarriers (3 x 8 bytes)
 constexpr uint32_t SS_RING_BYTES = SS_NSTAGE * SS_STAGE_BYTES;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
 constexpr uint32_t SS_K_SMALL = 4094;             // 16-bit index entries up to this k
-constexpr double SS_LOAD = 0.32;                  // index load factor (live keys / entries)
+constexpr double SS_LOAD = 0.24;  // index load factor (live keys / entries), before the slack fill
 constexpr int SS_MAX_KICKS = 200;
 
 // Index entry layout (runtime): slot in the low sb bits, fingerprint above. A slot field of all
@@ -148,29 +152,34 @@ struct SSLayout {
   uint32_t NB;
 };
 
-static double ss_load() {
-  const char* s = std::getenv("PSS_DEBUG_INDEX_LOAD");  // test hook: crowd the index
+// test hook: crowd the index (a 2-way, 2-choice cuckoo table holds up to ~0.89); 0 = unset
+static double ss_debug_load() {
+  const char* s = std::getenv("PSS_DEBUG_INDEX_LOAD");
   if (s) {
     double v = std::atof(s);
-    if (v > 0.05 && v <= 0.85) return v;  // 2-way 2-choice cuckoo holds up to ~0.89
+    if (v > 0.05 && v <= 0.85) return v;
   }
-  return SS_LOAD;
+  return 0.0;
+}
+static uint32_t ss_buckets(uint32_t k, double load) {
+  return (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * load)));
 }
 
-static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed) {
+static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed, uint32_t NB) {
   SSLayout L;
   const size_t KP = align_up(k, 32);
-  L.NB = (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * ss_load())));
+  L.NB = NB;
   Bump b;
   b.al = 16;  // every slot-indexed array holds exactly k entries (slots are < k)
   L.keys = b.take<unsigned char>((size_t)k * kb);
   L.cnt = b.take<uint32_t>(k);
   L.err = packed ? L.cnt : b.take<uint32_t>(k);
-  L.pos = b.take<unsigned char>((size_t)k * (eb == 2 ? 2 : 4));
+  // packed counters carry their index position in the top two bits (bucket choice, way)
+  L.pos = packed ? L.cnt : b.take<unsigned char>((size_t)k * (eb == 2 ? 2 : 4));
   L.bm = b.take<uint32_t>(KP / 32 + 2);
   L.vic = b.take<uint32_t>(32);
   L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
-  L.total = align_up(b.bytes(), 128);
+  L.total = b.bytes();  // a multiple of 16
   return L;
 }
 
@@ -209,9 +218,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 
   KT* ring = reinterpret_cast<KT*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SS_RING_BYTES);
-  unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + 64;
+  unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + SS_BAR_BYTES;
   KT* keys = reinterpret_cast<KT*>(st);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);  // count (| err << cb if PACKED)
+  // count; if PACKED also err << cb and the index position of the slot's entry in bits 30-31
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);
   PT* pos = reinterpret_cast<PT*>(st + a.o_pos);               // index entry of each slot
   uint32_t* err = reinterpret_cast<uint32_t*>(st + a.o_err);
   uint32_t* bm = reinterpret_cast<uint32_t*>(st + a.o_bm);
@@ -225,6 +235,17 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   const uint32_t kw = (k + 31u) / 32u;
   const uint32_t cb = a.cb;
   const uint32_t CM = PACKED ? ((1u << cb) - 1u) : 0xffffffffu;
+  constexpr uint32_t POSM = 3u << 30;
+  // index position bits of entry fi of a key whose first bucket is b1: (fi in b2) << 31 | way << 30
+  auto pos_bits = [](uint32_t fi, uint32_t b1) -> uint32_t {
+    return fi == 0xffffffffu ? 0u : (((fi >> 1) != b1 ? 2u : 0u) | (fi & 1u)) << 30;
+  };
+  auto set_pos = [&](uint32_t cv, uint32_t idx, uint32_t b1) {
+    if (PACKED)
+      cnt[cv] = (cnt[cv] & ~POSM) | pos_bits(idx, b1);
+    else
+      pos[cv] = (PT)idx;
+  };
   const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
   const uint64_t nfloor = aligned ? (n & ~(uint64_t)(E - 1)) : 0;
 
@@ -278,14 +299,14 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t fi = free_entry(f0, f1, f2, f3, b1, b2);
         if (fi != 0xffffffffu) {
           T[fi] = en.make(fp, cv);
-          pos[cv] = (PT)fi;
+          set_pos(cv, fi, b1);
           return true;
         }
         const uint32_t kb = (b1 != prev) ? b1 : b2;
         const uint32_t idx = 2 * kb + ((step ^ (cv & 1)) & 1);
         const ET e = T[idx];
         T[idx] = en.make(fp, cv);
-        pos[cv] = (PT)idx;
+        set_pos(cv, idx, b1);
         cv = en.slot(e);
         cx = keys[cv];
         prev = kb;
@@ -316,8 +337,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       if (tryfi) *tp = mine;
       __syncwarp();
       const bool won = tryfi && *tp == mine;
-      PT* const pp = pos + v;
-      if (won) *pp = (PT)fi;
+      if (!PACKED) {  // packed counters were written with the position bits of fi
+        PT* const pp = pos + v;
+        if (won) *pp = (PT)fi;
+      }
       uint32_t need = __ballot_sync(PSS_FULL, ins && !won);
       SS_STAT(2, __popc(need));
       SS_STAT(10, __popc(__ballot_sync(PSS_FULL, ins && fi == 0xffffffffu)));
@@ -387,7 +410,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 
       // lookup of x: slot s (-1 if not monitored), its packed count ce, the first free entry fi
       // of its buckets (insert target) and its fingerprint fp
-      auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp) {
+      auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp,
+                        uint32_t& fbits) {
         uint32_t b1, b2;
         key_hash<ET>(en, x, seed, NB, b1, b2, fp);
         ET e0, e1, e2, e3;
@@ -431,6 +455,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
           }
         }
         fi = free_entry(e0, e1, e2, e3, b1, b2);
+        fbits = PACKED ? pos_bits(fi, b1) : 0u;
       };
 
       uint32_t q = 0;  // items consumed
@@ -443,8 +468,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const KT x = ring[(roff + q + lane) % RING];
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
         int32_t s;
-        uint32_t ce, fi, fp;
-        lookup(x, act, s, ce, fi, fp);
+        uint32_t ce, fi, fp, fbits;
+        lookup(x, act, s, ce, fi, fp, fbits);
         const bool hit = s >= 0;
         const bool leader = act && (grp & ltm) == 0;
         const uint32_t missL = __ballot_sync(PSS_FULL, leader && !hit);
@@ -459,7 +484,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t v = size + __popc(missL & ltm);
         if (ins) {
           keys[v] = x;
-          cnt[v] = mult;
+          cnt[v] = mult | fbits;
           if (!PACKED) err[v] = 0;
         }
         const uint32_t grow = __popc(missL & pm);
@@ -502,11 +527,21 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         if (((wb >> lane) & 1u) && rb < 32) vic[rb] = w0 * 32 + 32 + lane;
         __syncwarp();
         const uint32_t myvic = vic[lane];
-        const uint32_t myop = pos[lane < navail ? myvic : 0];
+        uint32_t myop;
+        if (PACKED) {  // the victim's entry: its key's bucket pair and the position bits
+          const uint32_t tv = lane < navail ? myvic : 0;
+          const KT vk = keys[tv];
+          const uint32_t vc = cnt[tv];
+          uint32_t vb1, vb2, vfp;
+          key_hash<ET>(en, vk, seed, NB, vb1, vb2, vfp);
+          myop = 2 * ((vc >> 31) ? vb2 : vb1) + ((vc >> 30) & 1u);
+        } else {
+          myop = pos[lane < navail ? myvic : 0];
+        }
 
         int32_t s;
-        uint32_t ce, fi, fp;
-        lookup(x, act, s, ce, fi, fp);
+        uint32_t ce, fi, fp, fbits;
+        lookup(x, act, s, ce, fi, fp, fbits);
         SS_TICK(ph2, tk, ce ^ (uint32_t)s ^ myop);
         const uint32_t grp = grp_all & amask;
         const bool hit = s >= 0;
@@ -553,7 +588,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const bool ev = inpre && !hit;
         const uint32_t v = __shfl_sync(PSS_FULL, myvic, rank & 31u);
         const uint32_t op = __shfl_sync(PSS_FULL, myop, rank & 31u);
-        const uint32_t vnew = PACKED ? ((m + mult) | (m << cb)) : (m + mult);
+        const uint32_t vnew = PACKED ? ((m + mult) | (m << cb) | fbits) : (m + mult);
         ET* const tdel = T + op;
         KT* const kptr = keys + v;
         uint32_t* const vptr = cnt + v;
@@ -597,7 +632,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       const uint32_t ce = cnt[t];
       oi[t] = keys[t];
       oc[t] = ce & CM;
-      oe[t] = PACKED ? ce >> cb : err[t];
+      oe[t] = PACKED ? (ce & ~POSM) >> cb : err[t];
     }
     if (lane == 0) a.sizes[r] = size;
     __syncwarp();
@@ -617,10 +652,17 @@ struct SSPlan {
 template <typename KT, typename ET, bool G, bool PK>
 static int ss_blocks_per_sm(size_t smem) {
   auto kern = ss_summarize_kernel<KT, ET, G, PK>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem);
-  return nb > 0 ? nb : 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return nb;  // 0: does not fit
 }
 
 static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
@@ -629,34 +671,54 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   const uint64_t Lmax = (n + P - 1) / P;
   p.cb = 1;
   while (p.cb < 32 && (1ull << p.cb) <= Lmax) ++p.cb;
-  p.packed = p.cb < 32 && (Lmax / k) < (1ull << (32 - p.cb));
+  p.packed = p.cb < 30 && (Lmax / k) < (1ull << (30 - p.cb));  // bits 30-31: index position
   // 16-bit entries: the slot field's all-ones value must exceed k - 1
   uint32_t sb = 1;
   while ((1u << sb) - 1u < k) ++sb;
-  SSLayout Ls = ss_layout(k, kb, 2, p.packed);
+  const double dl = ss_debug_load();
+  uint32_t NB = ss_buckets(k, dl > 0 ? dl : SS_LOAD);
+  SSLayout Ls = ss_layout(k, kb, 2, p.packed, NB);
   p.gstate = k > SS_K_SMALL || Ls.total > SS_SMEM_STATE_MAX;
   if (!p.gstate) {
     p.sb = sb;
     p.fmask = (1u << (16 - sb)) - 1u;
+    size_t pad = 0;
+    if (const char* ps = std::getenv("PSS_DEBUG_SMEM_PAD"))  // experiment hook: fewer warps/SM
+      pad = (size_t)std::atoll(ps);
+    auto smem_of = [&](const SSLayout& L) { return SS_RING_BYTES + SS_BAR_BYTES + L.total + pad; };
+    auto blocks = [&](size_t smem) {
+      if (p.packed)
+        return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(smem)
+                       : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(smem);
+      return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(smem)
+                     : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem);
+    };
+    const int nb = blocks(smem_of(Ls));
+    // The shared memory left over at this occupancy goes to the index: the largest bucket count
+    // that keeps `nb` warps per SM (fewer fingerprint collisions and serial inserts).
+    if (dl == 0 && nb > 0) {
+      uint32_t lo = NB, hi = 2 * NB;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (blocks(smem_of(ss_layout(k, kb, 2, p.packed, mid))) >= nb)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      NB = lo;
+      Ls = ss_layout(k, kb, 2, p.packed, NB);
+    }
     p.L = Ls;
-    p.smem = SS_RING_BYTES + 64 + Ls.total;
-    if (const char* pad = std::getenv("PSS_DEBUG_SMEM_PAD"))  // experiment hook: fewer warps/SM
-      p.smem += (size_t)std::atoll(pad);
-    int nb;
-    if (p.packed)
-      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(p.smem)
-                   : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(p.smem);
-    else
-      nb = kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(p.smem)
-                   : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(p.smem);
-    p.grid = (int)std::min<uint64_t>(P, (uint64_t)nb * d.sms);
+    p.smem = smem_of(Ls);
+    blocks(p.smem);  // leaves the kernel's shared-memory attribute at the chosen size
+    p.grid = (int)std::min<uint64_t>(P, (uint64_t)std::max(nb, 1) * d.sms);
     p.slots = (int)std::min<uint64_t>((uint64_t)nb * d.sms, 1u << 30);
   } else {
     p.packed = false;
     p.sb = 32;
     p.fmask = 0xffffffffu;
-    p.L = ss_layout(k, kb, 8, false);
-    p.smem = SS_RING_BYTES + 64;
+    p.L = ss_layout(k, kb, 8, false, ss_buckets(k, dl > 0 ? dl : 0.32));
+    p.smem = SS_RING_BYTES + SS_BAR_BYTES;
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
     p.slots = 8 * d.sms;
   }
