@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="profiling runs only: skip the end-to-end leg (e2e is then null)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     return ap.parse_args()
 
@@ -281,9 +283,9 @@ def main():
     assert (counts >= thr).all() and (np.diff(counts.astype(np.int64)) <= 0).all()
 
     # ---- end to end: host (pinned) keys -> H2D -> path -> D2H of the answer, every step
-    E = args.e2e_steps or min(K, 5)
+    E = 0 if args.no_e2e else (args.e2e_steps or min(K, 5))
     e2e_ms = []
-    for i in range(E + 1):
+    for i in range(E + 1 if E else 0):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         if pg is not None:
@@ -294,7 +296,7 @@ def main():
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(a.elapsed_time(b))
-    e2e = statistics.median(e2e_ms)
+    e2e = statistics.median(e2e_ms) if e2e_ms else float("nan")
     if pg is not None:
         t = torch.tensor([e2e], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -324,9 +326,10 @@ def main():
             "hbm_frac_of_8TBs_summarize_merge": round(
                 n * kb / ((statistics.mean(per["summarize"]) + statistics.mean(per["merge"])) * 1e-3) / 8e12, 4),
             "roofline": roof,
-            "e2e": {"value": round(world * n / (e2e * 1e-3) / 1e9, 3), "unit": "Gitems/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": round(e2e, 3), "api": runner.host_api},
+            "e2e": None if not e2e_ms else {
+                "value": round(world * n / (e2e * 1e-3) / 1e9, 3), "unit": "Gitems/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e, 3), "api": runner.host_api},
             "gpu_launches": runner.launches_per_step * K,
             "clocks": clk.summary(),
             "result_len": ln}
