@@ -110,11 +110,12 @@ __device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT 
                                             uint32_t logT, bool perfect) {
   uint32_t h1, h2;
   vhash(x, seed, logT, h1, h2);
+  // an empty entry's index is 0xffffffff, so a key equal to its filler still finds nothing
   const typename VEnt<KT>::T a = tab[h1];
-  const uint32_t ia = (!VEnt<KT>::empty(a) && VEnt<KT>::key(a) == x) ? VEnt<KT>::idx(a) : 0xffffffffu;
+  const uint32_t ia = VEnt<KT>::key(a) == x ? VEnt<KT>::idx(a) : 0xffffffffu;
   if (perfect) return ia;
   const typename VEnt<KT>::T b = tab[h2];
-  const uint32_t ib = (!VEnt<KT>::empty(b) && VEnt<KT>::key(b) == x) ? VEnt<KT>::idx(b) : 0xffffffffu;
+  const uint32_t ib = VEnt<KT>::key(b) == x ? VEnt<KT>::idx(b) : 0xffffffffu;
   return min(ia, ib);
 }
 template <typename KT>
@@ -223,9 +224,10 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
                                             const typename VEnt<KT>::T* tab, uint32_t seed,
                                             uint32_t logT, uint32_t* lw, uint32_t* wc,
                                             unsigned long long* acc, uint64_t wid,
-                                            uint64_t nwarps) {
+                                            uint64_t nwarps, uint32_t nc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t ltm = lanemask_lt();
+  uint32_t* const lwl = lw + lane;
 #if PSS_VT_EXP == 2 || PSS_VT_EXP == 3  // timing experiment: no table lookup
   auto look = [&](KT x) { return (uint32_t)x & 31u; };
 #else
@@ -236,8 +238,9 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
   auto count1 = [&](uint32_t j) { sink += j; };
 #else
   auto count1 = [&](uint32_t j) {
-    if (MODE == 0) {
-      if (j != 0xffffffffu) red_shared_add(lw + (j >> 1) * 32 + lane, 1u << ((j & 1u) << 4));
+    if (MODE == 0) {  // no candidate: counted in the dummy counter nc (no branch)
+      const uint32_t jj = min(j, nc);
+      red_shared_add(lwl + (jj >> 1) * 32, 1u << ((jj & 1u) << 4));
     } else {
       const uint32_t g = __match_any_sync(PSS_FULL, j);
       if ((g & ltm) == 0 && j != 0xffffffffu) {
@@ -273,18 +276,24 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
     const uint64_t va = vb + u * stride + lane;
     q[u] = va < nvec ? __ldg(V + va) : make_uint4(0, 0, 0, 0);
   }
-  // steady state: this batch and the next one lie entirely inside A, no bounds checks
-  for (; vb + 2 * U * stride <= nvec; vb += U * stride) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) nq[u] = __ldg(V + vb + (U + u) * stride + lane);
+  // steady state, two batches per trip (q and nq alternate, no register copies): the batches
+  // being loaded lie entirely inside A, no bounds checks
+  auto process = [&](const uint4(&b)[U]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const KT* xs = reinterpret_cast<const KT*>(&q[u]);
+      const KT* xs = reinterpret_cast<const KT*>(&b[u]);
 #pragma unroll
       for (uint32_t e = 0; e < E; ++e) count1(look(xs[e]));
     }
+  };
+  for (; vb + 3 * U * stride <= nvec; vb += 2 * U * stride) {
+    const uint4* p = V + vb + lane;
 #pragma unroll
-    for (int u = 0; u < U; ++u) q[u] = nq[u];
+    for (int u = 0; u < U; ++u) nq[u] = __ldg(p + (U + u) * stride);
+    process(q);
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = __ldg(p + (2 * U + u) * stride);
+    process(nq);
   }
   for (; vb < nvec; vb += U * stride) {
     bool ok[U];
@@ -328,10 +337,10 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint32_t T = 1u << logT;
   const uint32_t warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
-  const int mode = (lane_ok && nc <= VLANE_MAX && T <= VT_SMEM) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
+  const int mode = (lane_ok && nc < VLANE_MAX && T <= VT_SMEM) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
   VT* stab = reinterpret_cast<VT*>(vsm);
   unsigned char* carea = vsm + (size_t)VT_SMEM * sizeof(VT);
-  const uint32_t ncw = (nc + 1) / 2;  // words per lane in mode 0
+  const uint32_t ncw = (nc + 2) / 2;  // words per lane in mode 0 (nc counters + the dummy)
   uint32_t* lw = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * ncw * 32;  // [cand/2][lane]
   uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;        // [cand]
   const bool tab_smem = T <= VT_SMEM;
@@ -348,15 +357,15 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint64_t nwarps = (uint64_t)gridDim.x * VWARPS;
   if (mode == 0) {
     if (perf)
-      verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps);
+      verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc);
     else
-      verify_scan<KT, 0, false>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps);
+      verify_scan<KT, 0, false>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc);
   } else {
     const VT* tab = tab_smem ? stab : gtab;
     if (mode == 1)
-      verify_scan<KT, 1, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps);
+      verify_scan<KT, 1, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps, nc);
     else
-      verify_scan<KT, 2, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps);
+      verify_scan<KT, 2, false>(A, n, tab, seed, logT, lw, wc, acc, wid, nwarps, nc);
   }
   if (mode != 2) {
     __syncthreads();
