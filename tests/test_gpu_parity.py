@@ -210,11 +210,26 @@ def test_verify_duplicates_absent_and_device_count(pss):
     torch.cuda.synchronize()
     assert ex3.cpu().numpy().tolist() == oracle.verify(A, many).tolist()
     # the three counting modes: per-lane counters, per-warp grouped counters, global atomics
-    for nc in (1, 128, 129, 500, 2048, 2049):
+    for nc in (1, 80, 81, 127, 128, 129, 500, 2048, 2049):
         c = np.unique(A)[:nc]
         ex4 = pss.pss_verify(dA, to_dev(c))
         torch.cuda.synchronize()
         assert ex4.cpu().numpy().tolist() == oracle.verify(A, c).tolist(), nc
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_verify_keys_equal_to_table_fillers(pss, kb):
+    """Empty table entries hold a filler key (all-ones for u32 tables, 0 for u64) with no
+    candidate index: stream items equal to the filler that are not candidates count nowhere."""
+    rng = np.random.default_rng(kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    filler = dt(0xFFFFFFFF) if kb == 4 else dt(0)
+    A = rng.integers(1, 50, size=300_007).astype(dt)
+    A[rng.random(A.size) < 0.3] = filler
+    for cand in (np.array([3, 7, 11], dt), np.arange(1, 100, dtype=dt), np.arange(1, 300, dtype=dt)):
+        ex = pss.pss_verify(to_dev(A), to_dev(cand))
+        torch.cuda.synchronize()
+        assert ex.cpu().numpy().tolist() == oracle.verify(A, cand).tolist(), cand.size
 
 
 def test_query_host_end_to_end(pss):
