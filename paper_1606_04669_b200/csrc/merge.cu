@@ -91,6 +91,15 @@ __device__ __forceinline__ void m_tick(int ph, uint32_t lv) {
 __device__ __forceinline__ void m_tick(int, uint32_t) {}
 #endif
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int NT>
 __device__ __forceinline__ uint32_t block_reduce(uint32_t v, uint32_t* red, bool is_min) {
   v = is_min ? __reduce_min_sync(PSS_FULL, v) : __reduce_add_sync(PSS_FULL, v);
@@ -408,194 +417,302 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
   m_tick(8, lv);
 }
 
-// EPT > 0: the sort keeps EPT elements per thread in registers; EPT == 0: shared-memory sort
+// loads of summaries: read-only path for inputs written by earlier launches (CG = false), L2
+// (bypassing L1, which is not coherent across SMs) for nodes written by other CTAs of the same
+// launch (CG = true)
+template <bool CG, typename T>
+__device__ __forceinline__ T ldx(const T* p) {
+  if constexpr (CG)
+    return __ldcg(p);
+  else
+    return __ldg(p);
+}
+
+// shared-memory views of one COMBINE's working set
+template <typename KT>
+struct CombSmem {
+  KT* ukey;
+  uint32_t* ucnt;
+  uint32_t* uerr;
+  uint8_t* dead;
+  uint32_t* ht;
+  uint32_t* xhi;
+  uint32_t* xidx;
+  KT* xlo;
+  uint32_t* red;
+  uint32_t* hist;
+};
+template <typename KT>
+__device__ __forceinline__ CombSmem<KT> comb_smem(const CombArgs& a, unsigned char* base,
+                                                  uint32_t* red, uint32_t* hist) {
+  CombSmem<KT> m;
+  m.ukey = reinterpret_cast<KT*>(base);
+  m.ucnt = reinterpret_cast<uint32_t*>(base + a.o_ucnt);
+  m.uerr = reinterpret_cast<uint32_t*>(base + a.o_uerr);
+  m.dead = reinterpret_cast<uint8_t*>(base + a.o_dead);
+  m.ht = reinterpret_cast<uint32_t*>(base + a.o_ht);
+  m.xhi = reinterpret_cast<uint32_t*>(base + a.o_x);
+  m.xidx = m.xhi + a.NP;
+  m.xlo = reinterpret_cast<KT*>(m.xidx + a.NP);
+  m.red = red;
+  m.hist = hist;
+  return m;
+}
+
+// One COMBINE (Alg. 2): node li of `ina` with node ri of `inb` (if has_r) into node blk of `o`.
+// EPT > 0: the root sort keeps EPT elements per thread in registers; EPT == 0: shared-memory sort
+template <typename KT, int NT, int EPT, bool CG>
+__device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
+                             const NodeRef& inb, uint32_t ri, bool has_r, const NodeOut& o,
+                             uint32_t blk, const CombSmem<KT>& sm, uint32_t lv) {
+  const uint32_t NP = a.NP;
+  const uint32_t k = a.k;
+  const uint32_t tid = threadIdx.x;
+  KT* const ukey = sm.ukey;
+  uint32_t* const ucnt = sm.ucnt;
+  uint32_t* const uerr = sm.uerr;
+  uint8_t* const dead = sm.dead;
+  uint32_t* const ht = sm.ht;
+  uint32_t* const xhi = sm.xhi;
+  uint32_t* const xidx = sm.xidx;
+  KT* const xlo = sm.xlo;
+  uint32_t* const red = sm.red;
+  uint32_t* const hist = sm.hist;
+  const uint32_t H2 = 1u << a.logH2, hmask = H2 - 1u;
+  (void)NP;
+  (void)xhi;
+  const uint32_t n1 = ldx<CG>(ina.sizes + li);
+  const uint32_t n2 = has_r ? ldx<CG>(inb.sizes + ri) : 0u;
+  const KT* i1 = reinterpret_cast<const KT*>(ina.items) + (size_t)li * k;
+  const uint32_t* c1 = ina.counts + (size_t)li * k;
+  const uint32_t* e1 = ina.errs + (size_t)li * k;
+  KT* oi = reinterpret_cast<KT*>(o.items) + (size_t)blk * k;
+  uint32_t* oc = o.counts + (size_t)blk * k;
+  uint32_t* oe = o.errs + (size_t)blk * k;
+
+  if (!has_r && !a.canon_single) {  // odd last node carried up unchanged (R6)
+    for (uint32_t t = tid; t < n1; t += NT) {
+      oi[t] = ldx<CG>(i1 + t);
+      oc[t] = ldx<CG>(c1 + t);
+      oe[t] = ldx<CG>(e1 + t);
+    }
+    if (tid == 0) o.sizes[blk] = n1;
+    return;
+  }
+  const KT* i2 = has_r ? reinterpret_cast<const KT*>(inb.items) + (size_t)ri * k : nullptr;
+  const uint32_t* c2 = has_r ? inb.counts + (size_t)ri * k : nullptr;
+  const uint32_t* e2 = has_r ? inb.errs + (size_t)ri * k : nullptr;
+
+  // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4). The loads of
+  // both summaries are issued before their stores.
+  uint32_t mn1 = 0xffffffffu, mn2 = 0xffffffffu;
+  for (uint32_t t = tid; t < max(n1, n2); t += NT) {
+    const bool h1 = t < n1, h2 = t < n2;
+    KT x1 = 0, x2 = 0;
+    uint32_t cc1 = 0, ee1 = 0, cc2 = 0, ee2 = 0;
+    if (h1) {
+      x1 = ldx<CG>(i1 + t);
+      cc1 = ldx<CG>(c1 + t);
+      ee1 = ldx<CG>(e1 + t);
+    }
+    if (h2) {
+      x2 = ldx<CG>(i2 + t);
+      cc2 = ldx<CG>(c2 + t);
+      ee2 = ldx<CG>(e2 + t);
+    }
+    if (h1) {
+      ukey[t] = x1;
+      ucnt[t] = cc1;
+      uerr[t] = ee1;
+      mn1 = min(mn1, cc1);
+    }
+    if (h2) {
+      ukey[n1 + t] = x2;
+      ucnt[n1 + t] = cc2;
+      uerr[n1 + t] = ee2;
+      dead[t] = 0;
+      mn2 = min(mn2, cc2);
+    }
+  }
+  for (uint32_t h = tid; h < H2; h += NT) ht[h] = 0xffffffffu;
+  mn1 = __reduce_min_sync(PSS_FULL, mn1);
+  mn2 = __reduce_min_sync(PSS_FULL, mn2);
+  __syncthreads();
+  if ((tid & 31u) == 0) {
+    red[tid >> 5] = mn1;
+    red[NT / 32 + (tid >> 5)] = mn2;
+  }
+  __syncthreads();
+  uint32_t m1r = 0xffffffffu, m2r = 0xffffffffu;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    m1r = min(m1r, red[w]);
+    m2r = min(m2r, red[NT / 32 + w]);
+  }
+  const uint32_t m1 = n1 == k ? m1r : 0u;
+  const uint32_t m2 = n2 == k ? m2r : 0u;
+  m_tick(0, lv);
+  // index S2's items (Find of Alg. 2 l.5)
+  for (uint32_t t = tid; t < n2; t += NT) {
+    uint32_t h = hslot(ukey[n1 + t], a.logH2);
+    while (atomicCAS(&ht[h], 0xffffffffu, t) != 0xffffffffu) h = (h + 1u) & hmask;
+  }
+  __syncthreads();
+  m_tick(1, lv);
+  // counters of S1: matched -> f1 + f2 and Remove from S2; else f1 + m2 (Alg. 2 l.4-13)
+  for (uint32_t t = tid; t < n1; t += NT) {
+    const KT x = ukey[t];
+    uint32_t h = hslot(x, a.logH2);
+    uint32_t j;
+    while ((j = ht[h]) != 0xffffffffu && ukey[n1 + j] != x) h = (h + 1u) & hmask;
+    if (j != 0xffffffffu) {
+      ucnt[t] += ucnt[n1 + j];
+      uerr[t] += uerr[n1 + j];
+      dead[j] = 1;
+    } else {
+      ucnt[t] += m2;
+      uerr[t] += m2;
+    }
+  }
+  __syncthreads();
+  m_tick(2, lv);
+  // remaining counters of S2: f2 + m1 (Alg. 2 l.14-18)
+  for (uint32_t t = tid; t < n2; t += NT)
+    if (!dead[t]) {
+      ucnt[n1 + t] += m1;
+      uerr[n1 + t] += m1;
+    }
+  __syncthreads();
+  m_tick(3, lv);
+  // Prune(k) (Alg. 2 l.19): order by (count desc, item asc), keep the first k (R5)
+  const uint32_t N = n1 + n2;
+  if (!a.sort_out) {  // internal tree node: the top-k set
+    select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, xidx, xlo, oi, oc,
+                              oe, o.sizes + blk, lv);
+    if (tid == 0) {
+#ifdef PSS_MSTATS
+      atomicAdd(&g_m_stats[lv & 15][15], 1ull);
+#endif
+    }
+    return;
+  }
+  if constexpr (EPT > 0) {
+    SE<KT> v[EPT];
+    uint32_t live = 0;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const uint32_t i = tid * EPT + j;
+      const bool valid = i < N && !(i >= n1 && dead[i - n1]);
+      v[j].hi = valid ? ~ucnt[i] : 0xffffffffu;  // valid counts are >= 1: ~count < all-ones
+      v[j].lo = valid ? ukey[i] : (KT)0;
+      v[j].idx = valid ? i : 0xffffffffu;
+      live += valid;
+    }
+    const uint32_t Lv = block_reduce<NT>(live, red, false);
+    bitonic<KT, NT, EPT>(v, xhi, xlo, xidx);
+    const uint32_t outn = min(Lv, k);
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const uint32_t i = tid * EPT + j;
+      if (i < outn) {
+        const uint32_t u = v[j].idx;
+        oi[i] = ukey[u];
+        oc[i] = ucnt[u];
+        oe[i] = uerr[u];
+      }
+    }
+    if (tid == 0) o.sizes[blk] = outn;
+  } else {
+    uint32_t live = 0;
+    for (uint32_t i = tid; i < NP; i += NT) {
+      const bool valid = i < N && !(i >= n1 && dead[i - n1]);
+      xhi[i] = valid ? ~ucnt[i] : 0xffffffffu;
+      xlo[i] = valid ? ukey[i] : (KT)0;
+      xidx[i] = valid ? i : 0xffffffffu;
+      live += valid;
+    }
+    const uint32_t Lv = block_reduce<NT>(live, red, false);
+    bitonic_smem<KT, NT>(NP, xhi, xlo, xidx);
+    const uint32_t outn = min(Lv, k);
+    for (uint32_t i = tid; i < outn; i += NT) {
+      const uint32_t u = xidx[i];
+      oi[i] = ukey[u];
+      oc[i] = ucnt[u];
+      oe[i] = uerr[u];
+    }
+    if (tid == 0) o.sizes[blk] = outn;
+  }
+}
+
 template <typename KT, bool G, int NT, int EPT>
 __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t red[3 * (NT / 32)];
   __shared__ uint32_t hist[260];
-  const uint32_t NP = a.NP;
-  const uint32_t k = a.k;
-  const uint32_t tid = threadIdx.x;
   unsigned char* base = G ? a.gscratch + (size_t)blockIdx.x * a.gstride : smem;
-  KT* ukey = reinterpret_cast<KT*>(base);
-  uint32_t* ucnt = reinterpret_cast<uint32_t*>(base + a.o_ucnt);
-  uint32_t* uerr = reinterpret_cast<uint32_t*>(base + a.o_uerr);
-  uint8_t* dead = reinterpret_cast<uint8_t*>(base + a.o_dead);
-  uint32_t* ht = reinterpret_cast<uint32_t*>(base + a.o_ht);
-  uint32_t* xhi = reinterpret_cast<uint32_t*>(base + a.o_x);
-  uint32_t* xidx = xhi + NP;
-  KT* xlo = reinterpret_cast<KT*>(xidx + NP);
-  const uint32_t H2 = 1u << a.logH2, hmask = H2 - 1u;
-
+  const CombSmem<KT> sm = comb_smem<KT>(a, base, red, hist);
   const uint32_t lv = ceil_log2(a.nblocks);
   for (uint32_t blk = blockIdx.x; blk < a.nblocks; blk += gridDim.x) {
     m_tick(-1, lv);
     const uint32_t li = blk * a.a_mul + a.a_add;
     const bool has_r = blk < a.nright;
     const uint32_t ri = blk * a.b_mul + a.b_add;
-    const uint32_t n1 = a.a.sizes[li];
-    const uint32_t n2 = has_r ? a.b.sizes[ri] : 0u;
-    const KT* i1 = reinterpret_cast<const KT*>(a.a.items) + (size_t)li * k;
-    const uint32_t* c1 = a.a.counts + (size_t)li * k;
-    const uint32_t* e1 = a.a.errs + (size_t)li * k;
-    KT* oi = reinterpret_cast<KT*>(a.o.items) + (size_t)blk * k;
-    uint32_t* oc = a.o.counts + (size_t)blk * k;
-    uint32_t* oe = a.o.errs + (size_t)blk * k;
+    combine_node<KT, NT, EPT, false>(a, a.a, li, a.b, ri, has_r, a.o, blk, sm, lv);
+    __syncthreads();
+  }
+}
 
-    if (!has_r && !a.canon_single) {  // odd last node carried up unchanged (R6)
-      for (uint32_t t = tid; t < n1; t += NT) {
-        oi[t] = i1[t];
-        oc[t] = c1[t];
-        oe[t] = e1[t];
-      }
-      if (tid == 0) a.o.sizes[blk] = n1;
-      continue;
-    }
-    const KT* i2 = has_r ? reinterpret_cast<const KT*>(a.b.items) + (size_t)ri * k : nullptr;
-    const uint32_t* c2 = has_r ? a.b.counts + (size_t)ri * k : nullptr;
-    const uint32_t* e2 = has_r ? a.b.errs + (size_t)ri * k : nullptr;
+// The internal levels of the tree in one persistent launch: CTAs take COMBINE tasks in level
+// order from a queue (task t = node t of the concatenated levels); a task waits until its
+// children's done flags are set, then runs and sets its own. Children always have smaller task
+// ids and are held by running CTAs, so there is no deadlock whatever the residency; levels
+// overlap, and there are no launch boundaries between them.
+struct TreeArgs {
+  CombArgs a;        // k, table sizes, shared-memory offsets
+  NodeRef leaves;
+  NodeOut nodes;     // every internal node, indexed by task id
+  uint32_t nlev;     // internal levels
+  uint32_t off[33];  // first task of each level; off[nlev] = number of tasks
+  uint32_t cin[32];  // input nodes of each level
+  uint32_t* flags;   // per task: 1 once its node is written
+  uint32_t* queue;
+};
 
-    // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4). The loads of
-    // both summaries are issued before their stores.
-    uint32_t mn1 = 0xffffffffu, mn2 = 0xffffffffu;
-    for (uint32_t t = tid; t < max(n1, n2); t += NT) {
-      const bool h1 = t < n1, h2 = t < n2;
-      KT x1 = 0, x2 = 0;
-      uint32_t cc1 = 0, ee1 = 0, cc2 = 0, ee2 = 0;
-      if (h1) {
-        x1 = __ldg(i1 + t);
-        cc1 = __ldg(c1 + t);
-        ee1 = __ldg(e1 + t);
-      }
-      if (h2) {
-        x2 = __ldg(i2 + t);
-        cc2 = __ldg(c2 + t);
-        ee2 = __ldg(e2 + t);
-      }
-      if (h1) {
-        ukey[t] = x1;
-        ucnt[t] = cc1;
-        uerr[t] = ee1;
-        mn1 = min(mn1, cc1);
-      }
-      if (h2) {
-        ukey[n1 + t] = x2;
-        ucnt[n1 + t] = cc2;
-        uerr[n1 + t] = ee2;
-        dead[t] = 0;
-        mn2 = min(mn2, cc2);
-      }
-    }
-    for (uint32_t h = tid; h < H2; h += NT) ht[h] = 0xffffffffu;
-    mn1 = __reduce_min_sync(PSS_FULL, mn1);
-    mn2 = __reduce_min_sync(PSS_FULL, mn2);
+template <typename KT, int NT>
+__global__ void __launch_bounds__(NT, 3) tree_kernel(const TreeArgs ta) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t red[3 * (NT / 32)];
+  __shared__ uint32_t hist[260];
+  __shared__ uint32_t task;
+  const CombSmem<KT> sm = comb_smem<KT>(ta.a, smem, red, hist);
+  const uint32_t ntasks = ta.off[ta.nlev];
+  const NodeRef nodes_in{ta.nodes.items, ta.nodes.counts, ta.nodes.errs, ta.nodes.sizes};
+  while (true) {
+    if (threadIdx.x == 0) task = atomicAdd(ta.queue, 1u);
     __syncthreads();
-    if ((tid & 31u) == 0) {
-      red[tid >> 5] = mn1;
-      red[NT / 32 + (tid >> 5)] = mn2;
+    const uint32_t t = task;
+    if (t >= ntasks) break;
+    uint32_t j = 0;
+    while (t >= ta.off[j + 1]) ++j;
+    const uint32_t i = t - ta.off[j];
+    const bool has_r = 2 * i + 1 < ta.cin[j];
+    const NodeRef& in = j == 0 ? ta.leaves : nodes_in;
+    const uint32_t base = j == 0 ? 0u : ta.off[j - 1];
+    if (j > 0 && threadIdx.x == 0) {  // acquire the children
+      const uint32_t* fl = ta.flags + base + 2 * i;
+      while (ld_acquire(fl) == 0 || (has_r && ld_acquire(fl + 1) == 0)) __nanosleep(64);
     }
     __syncthreads();
-    uint32_t m1r = 0xffffffffu, m2r = 0xffffffffu;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) {
-      m1r = min(m1r, red[w]);
-      m2r = min(m2r, red[NT / 32 + w]);
-    }
-    const uint32_t m1 = n1 == k ? m1r : 0u;
-    const uint32_t m2 = n2 == k ? m2r : 0u;
-    m_tick(0, lv);
-    // index S2's items (Find of Alg. 2 l.5)
-    for (uint32_t t = tid; t < n2; t += NT) {
-      uint32_t h = hslot(ukey[n1 + t], a.logH2);
-      while (atomicCAS(&ht[h], 0xffffffffu, t) != 0xffffffffu) h = (h + 1u) & hmask;
-    }
+    CombArgs a = ta.a;
+    a.sort_out = 0;
+    a.canon_single = 0;
+    combine_node<KT, NT, 0, true>(a, in, base + 2 * i, in, base + 2 * i + 1, has_r, ta.nodes, t,
+                                  sm, j);
     __syncthreads();
-    m_tick(1, lv);
-    // counters of S1: matched -> f1 + f2 and Remove from S2; else f1 + m2 (Alg. 2 l.4-13)
-    for (uint32_t t = tid; t < n1; t += NT) {
-      const KT x = ukey[t];
-      uint32_t h = hslot(x, a.logH2);
-      uint32_t j;
-      while ((j = ht[h]) != 0xffffffffu && ukey[n1 + j] != x) h = (h + 1u) & hmask;
-      if (j != 0xffffffffu) {
-        ucnt[t] += ucnt[n1 + j];
-        uerr[t] += uerr[n1 + j];
-        dead[j] = 1;
-      } else {
-        ucnt[t] += m2;
-        uerr[t] += m2;
-      }
+    if (threadIdx.x == 0) {  // release the node
+      __threadfence();
+      st_release(ta.flags + t, 1u);
     }
-    __syncthreads();
-    m_tick(2, lv);
-    // remaining counters of S2: f2 + m1 (Alg. 2 l.14-18)
-    for (uint32_t t = tid; t < n2; t += NT)
-      if (!dead[t]) {
-        ucnt[n1 + t] += m1;
-        uerr[n1 + t] += m1;
-      }
-    __syncthreads();
-    m_tick(3, lv);
-    // Prune(k) (Alg. 2 l.19): order by (count desc, item asc), keep the first k (R5)
-    const uint32_t N = n1 + n2;
-    if (!a.sort_out) {  // internal tree node: the top-k set
-      select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, xidx, xlo, oi, oc,
-                                oe, a.o.sizes + blk, lv);
-      if (tid == 0) {
-#ifdef PSS_MSTATS
-        atomicAdd(&g_m_stats[lv & 15][15], 1ull);
-#endif
-      }
-      continue;
-    }
-    if constexpr (EPT > 0) {
-      SE<KT> v[EPT];
-      uint32_t live = 0;
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) {
-        const uint32_t i = tid * EPT + j;
-        const bool valid = i < N && !(i >= n1 && dead[i - n1]);
-        v[j].hi = valid ? ~ucnt[i] : 0xffffffffu;  // valid counts are >= 1: ~count < all-ones
-        v[j].lo = valid ? ukey[i] : (KT)0;
-        v[j].idx = valid ? i : 0xffffffffu;
-        live += valid;
-      }
-      const uint32_t Lv = block_reduce<NT>(live, red, false);
-      bitonic<KT, NT, EPT>(v, xhi, xlo, xidx);
-      const uint32_t outn = min(Lv, k);
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) {
-        const uint32_t i = tid * EPT + j;
-        if (i < outn) {
-          const uint32_t u = v[j].idx;
-          oi[i] = ukey[u];
-          oc[i] = ucnt[u];
-          oe[i] = uerr[u];
-        }
-      }
-      if (tid == 0) a.o.sizes[blk] = outn;
-    } else {
-      uint32_t live = 0;
-      for (uint32_t i = tid; i < NP; i += NT) {
-        const bool valid = i < N && !(i >= n1 && dead[i - n1]);
-        xhi[i] = valid ? ~ucnt[i] : 0xffffffffu;
-        xlo[i] = valid ? ukey[i] : (KT)0;
-        xidx[i] = valid ? i : 0xffffffffu;
-        live += valid;
-      }
-      const uint32_t Lv = block_reduce<NT>(live, red, false);
-      bitonic_smem<KT, NT>(NP, xhi, xlo, xidx);
-      const uint32_t outn = min(Lv, k);
-      for (uint32_t i = tid; i < outn; i += NT) {
-        const uint32_t u = xidx[i];
-        oi[i] = ukey[u];
-        oc[i] = ucnt[u];
-        oe[i] = uerr[u];
-      }
-      if (tid == 0) a.o.sizes[blk] = outn;
-    }
-    __syncthreads();
   }
 }
 
@@ -622,6 +739,19 @@ static MPlan m_plan(int kb, uint32_t k, const DevInfo& d) {
   p.smem = p.g ? 0 : p.L.total;
   p.grid_cap = p.g ? 2 * d.sms : 1 << 30;
   return p;
+}
+
+static void fill_comb_args(CombArgs& a, int, uint32_t k, const MPlan& p, void* ws) {
+  a.k = k;
+  a.gscratch = p.g ? static_cast<unsigned char*>(ws) : nullptr;
+  a.gstride = p.L.total;
+  a.o_ucnt = p.L.ucnt;
+  a.o_uerr = p.L.uerr;
+  a.o_dead = p.L.dead;
+  a.o_ht = p.L.ht;
+  a.o_x = p.L.x;
+  a.logH2 = p.L.logH2;
+  a.NP = p.L.NP;
 }
 
 template <typename KT, bool G, int NT, int EPT>
@@ -655,16 +785,7 @@ static bool dispatch_comb(const CombArgs& a, int grid, const MPlan& p, cudaStrea
 static cudaError_t combine_run(int kb, uint32_t k, CombArgs a, void* ws, cudaStream_t s,
                                const DevInfo& d) {
   MPlan p = m_plan(kb, k, d);
-  a.k = k;
-  a.gscratch = p.g ? static_cast<unsigned char*>(ws) : nullptr;
-  a.gstride = p.L.total;
-  a.o_ucnt = p.L.ucnt;
-  a.o_uerr = p.L.uerr;
-  a.o_dead = p.L.dead;
-  a.o_ht = p.L.ht;
-  a.o_x = p.L.x;
-  a.logH2 = p.L.logH2;
-  a.NP = p.L.NP;
+  fill_comb_args(a, kb, k, p, ws);
   if (a.nblocks == 0) return cudaSuccess;
   const int grid = (int)std::min<uint32_t>(a.nblocks, (uint32_t)p.grid_cap);
   // Internal nodes (select, no sort): wide levels are throughput-bound and
@@ -729,20 +850,68 @@ cudaError_t combine_launch(int kb, uint32_t k, uint32_t count, const void* a_ite
   return combine_run(kb, k, a, ws, s, d);
 }
 
-// level buffers: A holds ceil(P/2) nodes, B ceil(P/4) nodes (levels alternate A, B, A, ...)
-size_t merge_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+// the fixed tree: internal levels (every COMBINE except the root), their first task ids and
+// input counts; c_final = nodes entering the root COMBINE (1 only when P == 1)
+struct TreePlan {
+  uint32_t nlev = 0, ntasks = 0, c_final = 0;
+  uint32_t off[33] = {};
+  uint32_t cin[32] = {};
+};
+static TreePlan tree_plan(uint32_t P) {
+  TreePlan t;
+  uint32_t c = P;
+  while (true) {
+    const uint32_t cout = (c + 1) / 2;
+    if (cout <= 1) break;
+    t.off[t.nlev] = t.ntasks;
+    t.cin[t.nlev] = c;
+    t.ntasks += cout;
+    ++t.nlev;
+    c = cout;
+  }
+  t.off[t.nlev] = t.ntasks;
+  t.c_final = c;
+  return t;
+}
+
+// workspace of pss_merge: every internal node (task order), sizes, done flags, the task queue,
+// and the global scratch of COMBINEs that do not fit shared memory
+struct TreeWs {
+  size_t items, counts, errs, sizes, flags, queue, scratch, total;
+};
+static TreeWs tree_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  const TreePlan t = tree_plan(P);
+  const size_t nn = std::max<uint32_t>(t.ntasks, 1);
+  TreeWs w;
   Bump b;
-  const size_t nA = (P + 1) / 2, nB = (P + 3) / 4;
-  b.take<unsigned char>(nA * k * kb);
-  b.take<uint32_t>(nA * k);
-  b.take<uint32_t>(nA * k);
-  b.take<uint32_t>(nA);
-  b.take<unsigned char>(nB * k * kb);
-  b.take<uint32_t>(nB * k);
-  b.take<uint32_t>(nB * k);
-  b.take<uint32_t>(nB);
-  b.take<unsigned char>(scratch_bytes(kb, k, d));
-  return b.bytes();
+  w.items = b.take<unsigned char>(nn * k * kb);
+  w.counts = b.take<uint32_t>(nn * k);
+  w.errs = b.take<uint32_t>(nn * k);
+  w.sizes = b.take<uint32_t>(nn);
+  w.flags = b.take<uint32_t>(nn);
+  w.queue = b.take<uint32_t>(1);
+  w.scratch = b.take<unsigned char>(scratch_bytes(kb, k, d));
+  w.total = b.bytes();
+  return w;
+}
+
+size_t merge_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  return tree_ws(kb, k, P, d).total;
+}
+
+template <typename KT>
+static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo& d,
+                               cudaStream_t s) {
+  constexpr int NT = 512;
+  auto kern = tree_kernel<KT, NT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, p.smem) != cudaSuccess ||
+      nb < 1)
+    nb = 1;
+  const int grid = (int)std::min<uint64_t>(ta.off[ta.nlev], (uint64_t)nb * d.sms);
+  kern<<<grid, NT, p.smem, s>>>(ta);
+  return cudaGetLastError();
 }
 
 cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
@@ -750,25 +919,17 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
                               void* r_items, uint32_t* r_counts, uint32_t* r_errs,
                               uint32_t* r_sizes, void* ws, cudaStream_t s, const DevInfo& d) {
   unsigned char* w = static_cast<unsigned char*>(ws);
-  Bump b;
-  const size_t nA = (P + 1) / 2, nB = (P + 3) / 4;
-  NodeOut bufA, bufB;
-  bufA.items = w + b.take<unsigned char>(nA * k * kb);
-  bufA.counts = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nA * k));
-  bufA.errs = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nA * k));
-  bufA.sizes = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nA));
-  bufB.items = w + b.take<unsigned char>(nB * k * kb);
-  bufB.counts = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nB * k));
-  bufB.errs = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nB * k));
-  bufB.sizes = reinterpret_cast<uint32_t*>(w + b.take<uint32_t>(nB));
-  void* scratch = w + b.take<unsigned char>(scratch_bytes(kb, k, d));
-
-  NodeRef cur{items, counts, errs, sizes};
+  const TreeWs L = tree_ws(kb, k, P, d);
+  const TreePlan t = tree_plan(P);
+  NodeOut nodes{w + L.items, reinterpret_cast<uint32_t*>(w + L.counts),
+                reinterpret_cast<uint32_t*>(w + L.errs), reinterpret_cast<uint32_t*>(w + L.sizes)};
+  void* scratch = w + L.scratch;
+  NodeRef leaves{items, counts, errs, sizes};
   NodeOut root{r_items, r_counts, r_errs, r_sizes};
   if (P == 1) {  // root = the only leaf, in canonical order = COMBINE(S, empty)
     CombArgs a{};
-    a.a = cur;
-    a.b = cur;
+    a.a = leaves;
+    a.b = leaves;
     a.o = root;
     a.a_mul = 1;
     a.b_mul = 1;
@@ -778,30 +939,60 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
     a.sort_out = 1;
     return combine_run(kb, k, a, scratch, s, d);
   }
-  uint32_t c = P;
-  int level = 0;
-  while (c > 1) {
-    const uint32_t cout = (c + 1) / 2;
-    NodeOut out = cout == 1 ? root : (level % 2 == 0 ? bufA : bufB);
-    CombArgs a{};
-    a.a = cur;
-    a.b = cur;
-    a.o = out;
-    a.a_mul = 2;
-    a.a_add = 0;
-    a.b_mul = 2;
-    a.b_add = 1;
-    a.nblocks = cout;
-    a.nright = c / 2;
-    a.canon_single = 0;
-    a.sort_out = cout == 1;  // internal nodes are top-k sets; the root is canonical (R5)
-    cudaError_t e = combine_run(kb, k, a, scratch, s, d);
-    if (e != cudaSuccess) return e;
-    cur = NodeRef{out.items, out.counts, out.errs, out.sizes};
-    c = cout;
-    ++level;
+  const MPlan p = m_plan(kb, k, d);
+  if (t.nlev > 0) {
+    if (!p.g) {  // all internal levels in one persistent launch
+      cudaError_t e = cudaMemsetAsync(w + L.flags, 0, (L.queue - L.flags) + sizeof(uint32_t), s);
+      if (e != cudaSuccess) return e;
+      TreeArgs ta{};
+      fill_comb_args(ta.a, kb, k, p, nullptr);
+      ta.leaves = leaves;
+      ta.nodes = nodes;
+      ta.nlev = t.nlev;
+      for (uint32_t i = 0; i <= t.nlev; ++i) ta.off[i] = t.off[i];
+      for (uint32_t i = 0; i < t.nlev; ++i) ta.cin[i] = t.cin[i];
+      ta.flags = reinterpret_cast<uint32_t*>(w + L.flags);
+      ta.queue = reinterpret_cast<uint32_t*>(w + L.queue);
+      e = kb == 4 ? launch_tree<uint32_t>(ta, p, d, s) : launch_tree<uint64_t>(ta, p, d, s);
+      if (e != cudaSuccess) return e;
+    } else {  // summaries too large for shared memory: one launch per level
+      for (uint32_t lv = 0; lv < t.nlev; ++lv) {
+        CombArgs a{};
+        a.a = lv == 0 ? leaves
+                      : NodeRef{nodes.items, nodes.counts, nodes.errs, nodes.sizes};
+        a.b = a.a;
+        a.o = NodeOut{static_cast<unsigned char*>(nodes.items) + (size_t)t.off[lv] * k * kb,
+                      nodes.counts + (size_t)t.off[lv] * k, nodes.errs + (size_t)t.off[lv] * k,
+                      nodes.sizes + t.off[lv]};
+        const uint32_t base = lv == 0 ? 0u : t.off[lv - 1];
+        a.a_mul = 2;
+        a.a_add = base;
+        a.b_mul = 2;
+        a.b_add = base + 1;
+        a.nblocks = t.off[lv + 1] - t.off[lv];
+        a.nright = t.cin[lv] / 2;
+        a.canon_single = 0;
+        a.sort_out = 0;
+        const cudaError_t e = combine_run(kb, k, a, scratch, s, d);
+        if (e != cudaSuccess) return e;
+      }
+    }
   }
-  return cudaSuccess;
+  // the root (canonical order, R5)
+  CombArgs a{};
+  const uint32_t base = t.nlev == 0 ? 0u : t.off[t.nlev - 1];
+  a.a = t.nlev == 0 ? leaves : NodeRef{nodes.items, nodes.counts, nodes.errs, nodes.sizes};
+  a.b = a.a;
+  a.o = root;
+  a.a_mul = 2;
+  a.a_add = base;
+  a.b_mul = 2;
+  a.b_add = base + 1;
+  a.nblocks = 1;
+  a.nright = t.c_final / 2;
+  a.canon_single = 0;
+  a.sort_out = 1;
+  return combine_run(kb, k, a, scratch, s, d);
 }
 
 // ---- K3: Pruned(global, n, k) -- the root is in canonical order, so candidates are a prefix

@@ -61,6 +61,20 @@ def allreduce_counts(exact: torch.Tensor, group=None) -> torch.Tensor:
     return exact
 
 
+def _merge_launches(P: int, k: int, kb: int) -> int:
+    """Kernels pss_merge launches (csrc/merge.cu): the root COMBINE, plus one persistent launch
+    for all internal levels when a COMBINE's working set fits shared memory (else one per level)."""
+    if P <= 2:
+        return 1
+    levels, c = 0, P
+    while (c + 1) // 2 > 1:
+        c = (c + 1) // 2
+        levels += 1
+    NP = max(256, 1 << (2 * k - 1).bit_length())
+    work = 2 * k * (kb + 8) + k + 4 * (1 << (2 * k - 1).bit_length()) + NP * (8 + kb)
+    return 1 + (1 if work <= 227 * 1024 - 2048 else levels)
+
+
 class Runner:
     """Preallocated buffers + one step of the path (see module docstring)."""
 
@@ -85,10 +99,8 @@ class Runner:
                     torch.empty((k,), dtype=torch.uint64, device=self.dev),
                     torch.zeros((1,), dtype=torch.uint32, device=self.dev))
         self.host_out = tuple(torch.empty_like(t, device="cpu").pin_memory() for t in self.out)
-        levels = max(1, math.ceil(math.log2(P))) if P > 1 else 1
-        top = max(1, math.ceil(math.log2(world))) if world > 1 else 0
-        # K1 + merge levels (+ top levels) + K3 + K4 (setup, scan, finalize) + K5
-        self.launches_per_step = 1 + levels + top + 1 + 3 + 1
+        self.launches_per_step = (1 + _merge_launches(P, k, kb) +
+                                  (_merge_launches(world, k, kb) if world > 1 else 0) + 1 + 3 + 1)
         self.host_api = "pss_query_host" if world == 1 else "H2D copy + step + D2H (torch)"
         self._kb = kb
 
