@@ -314,6 +314,11 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
     hist[258] = 0;
     hist[259] = 0;
   }
+  // radix passes alternate between two histograms: a pass clears the next one while it fills
+  // its own, so a pass needs two barriers instead of four
+  uint32_t* const hb = hist + 260;
+  uint32_t pb = 0;
+  for (uint32_t b = tid; b < 256; b += NT) hb[b] = 0;
   __syncthreads();
   uint32_t Lv = 0;
   mn = 0xffffffffu;
@@ -338,21 +343,21 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
       int shift = top / 8 * 8;
       uint32_t mask = shift >= 24 ? 0u : ~((1u << (shift + 8)) - 1u);
       C = mn & mask;
-      for (; shift >= 0; shift -= 8) {
-        for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
-        __syncthreads();
+      for (; shift >= 0; shift -= 8, ++pb) {
+        uint32_t* const cur = hb + 258 * (pb & 1u);
+        uint32_t* const nxt = hb + 258 * ((pb + 1) & 1u);
+        for (uint32_t b = tid; b < 256; b += NT) nxt[b] = 0;
         for (uint32_t i = tid; i < N; i += NT) {
           if (i >= n1 && dead[i - n1]) continue;
           const uint32_t c = ucnt[i];
-          if ((c & mask) == C) atomicAdd(&hist[(c >> shift) & 255u], 1u);
+          if ((c & mask) == C) atomicAdd(&cur[(c >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (tid < 32) radix_pick(hist, need, true);
+        if (tid < 32) radix_pick(cur, need, true);
         __syncthreads();
-        need -= hist[257];
-        C |= hist[256] << shift;
+        need -= cur[257];
+        C |= cur[256] << shift;
         mask |= 255u << shift;
-        __syncthreads();
       }
     }
     m_tick(6, lv);
@@ -381,20 +386,20 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
         K = kres;
       } else {
         KT kmask = 0;
-        for (int shift = 8 * (int)sizeof(KT) - 8; shift >= 0; shift -= 8) {
-          for (uint32_t b = tid; b < 256; b += NT) hist[b] = 0;
-          __syncthreads();
+        for (int shift = 8 * (int)sizeof(KT) - 8; shift >= 0; shift -= 8, ++pb) {
+          uint32_t* const cur = hb + 258 * (pb & 1u);
+          uint32_t* const nxt = hb + 258 * ((pb + 1) & 1u);
+          for (uint32_t b = tid; b < 256; b += NT) nxt[b] = 0;
           for (uint32_t j = tid; j < E; j += NT) {
             const KT x = tkey[j];
-            if ((x & kmask) == K) atomicAdd(&hist[(uint32_t)(x >> shift) & 255u], 1u);
+            if ((x & kmask) == K) atomicAdd(&cur[(uint32_t)(x >> shift) & 255u], 1u);
           }
           __syncthreads();
-          if (tid < 32) radix_pick(hist, need, false);
+          if (tid < 32) radix_pick(cur, need, false);
           __syncthreads();
-          need -= hist[257];
-          K |= (KT)hist[256] << shift;
+          need -= cur[257];
+          K |= (KT)cur[256] << shift;
           kmask |= (KT)255 << shift;
-          __syncthreads();
         }
       }
     }
@@ -648,7 +653,7 @@ template <typename KT, bool G, int NT, int EPT>
 __global__ void __launch_bounds__(NT) combine_kernel(const CombArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t red[3 * (NT / 32)];
-  __shared__ uint32_t hist[260];
+  __shared__ uint32_t hist[260 + 2 * 258];
   unsigned char* base = G ? a.gscratch + (size_t)blockIdx.x * a.gstride : smem;
   const CombSmem<KT> sm = comb_smem<KT>(a, base, red, hist);
   const uint32_t lv = ceil_log2(a.nblocks);
@@ -682,7 +687,7 @@ template <typename KT, int NT>
 __global__ void __launch_bounds__(NT, 3) tree_kernel(const TreeArgs ta) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t red[3 * (NT / 32)];
-  __shared__ uint32_t hist[260];
+  __shared__ uint32_t hist[260 + 2 * 258];
   __shared__ uint32_t task;
   const CombSmem<KT> sm = comb_smem<KT>(ta.a, smem, red, hist);
   const uint32_t ntasks = ta.off[ta.nlev];
