@@ -47,16 +47,32 @@ def gather_summaries(root: Summaries, group=None) -> Summaries:
                     torch.empty((world, root.k), dtype=root.counts.dtype, device=root.items.device),
                     torch.empty((world, root.k), dtype=root.errs.dtype, device=root.items.device),
                     torch.empty((world,), dtype=root.sizes.dtype, device=root.items.device))
+    host = _host_staged(root.items, group)
     for src, dst in ((root.items, out.items), (root.counts, out.counts), (root.errs, out.errs),
                      (root.sizes, out.sizes)):
-        parts = list(_as_signed(dst).reshape(world, -1).unbind(0))
-        dist.all_gather(parts, _as_signed(src).reshape(-1), group=group)
+        d = dst.cpu() if host else dst
+        parts = list(_as_signed(d).reshape(world, -1).unbind(0))
+        dist.all_gather(parts, _as_signed(src.cpu() if host else src).reshape(-1), group=group)
+        if host:
+            dst.copy_(d)
     return out
+
+
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo moves host tensors only: device tensors are staged through host memory (tests)."""
+    import torch.distributed as dist
+
+    return t.is_cuda and dist.get_backend(group) == "gloo"
 
 
 def allreduce_counts(exact: torch.Tensor, group=None) -> torch.Tensor:
     import torch.distributed as dist
 
+    if _host_staged(exact, group):
+        h = exact.cpu()
+        dist.all_reduce(_as_signed(h), op=dist.ReduceOp.SUM, group=group)
+        exact.copy_(h)
+        return exact
     dist.all_reduce(_as_signed(exact), op=dist.ReduceOp.SUM, group=group)
     return exact
 
