@@ -501,14 +501,17 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 #ifdef PSS_STATS
       long long tk = 0, ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0, ph5 = 0;
 #endif
-      while (q < L) {
-        const uint32_t nv = min(32u, L - q);
+      // one step; F: a full 32-item window (every step but the block's last), compiled separately
+      // so that the window-length predicates fold away
+      auto full_step = [&](auto full) {
+        constexpr bool F = decltype(full)::value;
+        const uint32_t nv = F ? 32u : min(32u, L - q);
         ensure(q + nv);
 #ifdef PSS_STATS
         tk = clock64();
 #endif
-        const bool act = lane < nv;
-        const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
+        const bool act = F || lane < nv;
+        const uint32_t amask = F || nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
         const KT x = ring[(roff + q + lane) % RING];
         // the match is issued first and its result first used after the lookups, so that its
         // latency (it grows with the number of distinct keys) overlaps them
@@ -614,7 +617,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         }
         __syncwarp();
         SS_TICK(ph5, tk, bmcount);
-      }
+      };
+      while (q + 32 <= L) full_step(std::true_type{});
+      while (q < L) full_step(std::false_type{});
 #ifdef PSS_STATS
       SS_STAT(11, ph1);
       SS_STAT(12, ph2);
