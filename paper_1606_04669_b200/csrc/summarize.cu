@@ -68,7 +68,10 @@ namespace pss {
 #endif
 
 // per-warp TMA ring: 3 stages of 512 bytes (a step spans at most two stages; one more in flight)
-constexpr uint32_t SS_NSTAGE = 3;
+#ifndef PSS_SS_NSTAGE
+#define PSS_SS_NSTAGE 3
+#endif
+constexpr uint32_t SS_NSTAGE = PSS_SS_NSTAGE;
 #ifndef PSS_SS_STAGE_BYTES
 #define PSS_SS_STAGE_BYTES 512
 #endif
