@@ -191,10 +191,14 @@ def pss_combine(a: Summaries, b: Summaries, out: Summaries | None = None,
     return out
 
 
-def pss_prune(root: Summaries, n: int, stream=None):
-    """Pruned(global, n, k) (Alg. 1 l.8-9): (candidates[k] device keys, n_cand[1] device uint32)."""
-    cand = torch.empty((root.k,), dtype=root.items.dtype, device=root.items.device)
-    n_cand = torch.zeros((1,), dtype=torch.uint32, device=root.items.device)
+def pss_prune(root: Summaries, n: int, stream=None, out=None):
+    """Pruned(global, n, k) (Alg. 1 l.8-9): (candidates[k] device keys, n_cand[1] device uint32).
+    `out` = preallocated (cand, n_cand); the kernel writes n_cand, so neither needs clearing."""
+    if out is not None:
+        cand, n_cand = out
+    else:
+        cand = torch.empty((root.k,), dtype=root.items.dtype, device=root.items.device)
+        n_cand = torch.empty((1,), dtype=torch.uint32, device=root.items.device)
     c = root._c()
     _check("pss_prune", _lib.pss_prune(ctypes.byref(c), n, cand.data_ptr(), n_cand.data_ptr(),
                                        _stream(stream)))

@@ -110,6 +110,8 @@ class Runner:
                  pss_workspace_bytes(OP_VERIFY, n, k, 1, key_type))
         self.ws = torch.empty((ws,), dtype=torch.uint8, device=self.dev)
         self.exact = torch.zeros((k,), dtype=torch.uint64, device=self.dev)
+        self.cand = (torch.empty((k,), dtype=_key_dtype(key_type), device=self.dev),
+                     torch.empty((1,), dtype=torch.uint32, device=self.dev))
         kd = _key_dtype(key_type)
         self.out = (torch.empty((k,), dtype=kd, device=self.dev),
                     torch.empty((k,), dtype=torch.uint64, device=self.dev),
@@ -134,7 +136,7 @@ class Runner:
             pss_merge(gathered, out=self.top, workspace=self.ws)
         if ev is not None:
             ev[2].record(s)
-        cand, n_cand = pss_prune(self.top, n_global)
+        cand, n_cand = pss_prune(self.top, n_global, out=self.cand)
         exact = pss_verify(A, cand, n_cand, out=self.exact, workspace=self.ws)
         if self.world > 1:
             allreduce_counts(self.exact, self.group)
