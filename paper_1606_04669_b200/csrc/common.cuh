@@ -107,6 +107,20 @@ __device__ __forceinline__ bool canon_before(uint32_t ca, KT ka, uint32_t cb, KT
   return ca > cb || (ca == cb && ka < kb);
 }
 
+// A kernel's dynamic shared-memory limit is a per-function, process-wide attribute: it is always
+// raised to the device maximum (never to the size of one launch), so callers on concurrent
+// streams with different sizes cannot race on it. Occupancy depends on each launch's own size.
+template <typename Kern>
+inline cudaError_t allow_max_smem(Kern kern, const DevInfo& d) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             d.smem_optin - (int)fa.sharedSizeBytes);
+  if (e != cudaSuccess) (void)cudaGetLastError();
+  return e;
+}
+
 // ---- host-side bump allocator over a workspace
 struct Bump {
   size_t off = 0;

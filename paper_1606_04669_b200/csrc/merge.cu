@@ -762,7 +762,7 @@ static void fill_comb_args(CombArgs& a, int, uint32_t k, const MPlan& p, void* w
 template <typename KT, bool G, int NT, int EPT>
 static void launch_comb(const CombArgs& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = combine_kernel<KT, G, NT, EPT>;
-  if (!G) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!G) allow_max_smem(kern, dev_info());
   kern<<<grid, NT, G ? 0 : smem, s>>>(a);
 }
 
@@ -909,7 +909,7 @@ static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo
                                cudaStream_t s) {
   constexpr int NT = 512;
   auto kern = tree_kernel<KT, NT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  allow_max_smem(kern, d);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, p.smem) != cudaSuccess ||
       nb < 1)

@@ -658,13 +658,9 @@ struct SSPlan {
 };
 
 template <typename KT, typename ET, bool G, bool PK>
-static int ss_blocks_per_sm(size_t smem) {
+static int ss_blocks_per_sm(size_t smem, const DevInfo& d) {
   auto kern = ss_summarize_kernel<KT, ET, G, PK>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess) {
-    (void)cudaGetLastError();
-    return 0;
-  }
+  if (smem > (size_t)d.smem_optin || allow_max_smem(kern, d) != cudaSuccess) return 0;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -696,10 +692,10 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     auto smem_of = [&](const SSLayout& L) { return SS_RING_BYTES + SS_BAR_BYTES + L.total + pad; };
     auto blocks = [&](size_t smem) {
       if (p.packed)
-        return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(smem)
-                       : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(smem);
-      return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(smem)
-                     : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem);
+        return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(smem, d)
+                       : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(smem, d);
+      return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(smem, d)
+                     : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem, d);
     };
     const int nb = blocks(smem_of(Ls));
     // The shared memory left over at this occupancy goes to the index: the largest bucket count
@@ -718,7 +714,6 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     }
     p.L = Ls;
     p.smem = smem_of(Ls);
-    blocks(p.smem);  // leaves the kernel's shared-memory attribute at the chosen size
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)std::max(nb, 1) * d.sms);
     p.slots = (int)std::min<uint64_t>((uint64_t)nb * d.sms, 1u << 30);
   } else {

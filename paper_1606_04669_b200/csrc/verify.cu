@@ -414,7 +414,7 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
   if (cap == 0) return cudaSuccess;
   verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, ctl);
   const size_t smem = (size_t)VT_SMEM * sizeof(VT) + VC_BYTES;
-  cudaFuncSetAttribute(verify_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem(verify_kernel<KT>, d);
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<KT>, VTHREADS, smem);
   if (nb < 1) nb = 1;
