@@ -175,6 +175,60 @@ pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type k
                           uint32_t P, void* h_out_items, uint64_t* h_out_counts,
                           uint32_t* h_out_len, void* d_ws, size_t ws_bytes, cudaStream_t stream);
 
+/*
+ * ---- On-line ingestion -------------------------------------
+ * The stream is cut into consecutive leaves of leaf_len items (Alg. 1's blocks, with a
+ * fixed length instead of floor(r n / P) bounds; the last leaf may be shorter), each summarized by
+ * sequential Space Saving (R1, R2), and its summary at any point is the fixed balanced
+ * binary COMBINE tree (R6; Alg. 2) over the leaves so far. When the number of items is
+ * a multiple of leaf_len, that is bit for bit the root pss_summarize + pss_merge compute with
+ * P = n / leaf_len. The tree is maintained incrementally (a binary counter of complete subtrees)
+ * and nothing is re-read: this is the on-line setting of P:42, so candidates come from pss_prune
+ * on the root (no verification pass; no false negatives).
+ *
+ * State: a pss_stream (host struct, caller-owned; written by pss_stream_init and every feed) plus
+ * a device workspace of pss_stream_workspace_bytes(...) bytes that holds the subtree stack, the
+ * partial leaf, a batch of leaf summaries and the host-feed buffers. A stream is used by one host
+ * thread and one CUDA stream at a time. Stream length: N + floor(N/k) <= 2^32 - 1 (u32 counters,
+ * R9), i.e. N <= floor((2^32 - 1) k / (k + 1)); a feed past it returns PSS_ERR_UNSUPPORTED and
+ * changes nothing.
+ */
+typedef struct {
+  int32_t key_type;      /* pss_key_type */
+  uint32_t k;            /* counters per summary */
+  uint32_t leaf_len;     /* items per leaf, >= 1 */
+  uint32_t batch_leaves; /* leaves summarized per K1 launch (workspace capacity), >= 1 */
+  uint64_t n_seen;       /* items ingested so far */
+  void* d_ws;            /* device workspace (caller-owned) */
+  size_t ws_bytes;
+} pss_stream;
+
+/* Bytes of device workspace a stream needs (0 for invalid arguments). Dominated by
+ * 2 * batch_leaves * leaf_len keys of host-feed buffers and batch_leaves leaf summaries. */
+size_t pss_stream_workspace_bytes(pss_key_type kt, uint32_t k, uint32_t leaf_len,
+                                  uint32_t batch_leaves);
+
+/* Initialise *st as an empty stream (host only, launches nothing; the workspace need not be
+ * cleared). INVALID_ARG for null pointers, k < 2, leaf_len == 0, batch_leaves == 0 or a bad key
+ * type; UNSUPPORTED for k > PSS_MAX_K or batch_leaves * leaf_len > 2^31; WORKSPACE_TOO_SMALL. */
+pss_status pss_stream_init(pss_stream* st, pss_key_type kt, uint32_t k, uint32_t leaf_len,
+                           uint32_t batch_leaves, void* d_ws, size_t ws_bytes);
+
+/* Append len keys from DEVICE memory (read-only; may be reused once the work enqueued on `stream`
+ * is done). Any len, including 0 and pieces that split a leaf. Updates st->n_seen. */
+pss_status pss_stream_feed(pss_stream* st, const void* d_chunk, uint64_t len, cudaStream_t stream);
+
+/* Append len keys from HOST memory (pinned recommended): copied in pieces of batch_leaves *
+ * leaf_len keys on a private copy stream into two alternating device buffers, each piece ingested
+ * on `stream` as soon as it has landed (the copy of piece g + 1 overlaps the kernels of piece g).
+ * h_chunk must stay valid and unmodified until `stream` is synchronised. */
+pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t len,
+                                cudaStream_t stream);
+
+/* The summary of the stream so far (the R6 tree over its leaves, the partial leaf included), in
+ * canonical order (R5) into root (count 1, same k and key type). Does not change the stream. */
+pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream_t stream);
+
 /* Human-readable name of a status. */
 const char* pss_status_string(pss_status s);
 

@@ -223,3 +223,19 @@ def pipeline(A, k: int, P: int, threads: int = 1) -> Pipeline:
     cand = prune(root, A.size, k)
     exact = verify(A, cand)
     return Pipeline(L, root, cand, exact, result(cand, exact, A.size, k))
+
+
+def stream_bounds(n: int, leaf_len: int) -> list[tuple[int, int]]:
+    """Leaves of the on-line stream (reading R14): consecutive blocks of leaf_len
+    items, the last one possibly shorter (Alg. 1's blocks, with a fixed length)."""
+    return [(lo, min(lo + leaf_len, n)) for lo in range(0, n, leaf_len)]
+
+
+def stream_root(A, k: int, leaf_len: int) -> Summary:
+    """Summary of a stream fed on-line (on-line setting PAPER.md:42): Space Saving
+    on every leaf, then the fixed binary tree over the leaves (Alg. 1 line 7, R6),
+    computed level by level exactly as ``tree`` does. An empty stream has an empty summary."""
+    A, _ = _keys(A)
+    if A.size == 0:
+        return empty_summary()
+    return tree([space_saving(A, k, lo, hi) for lo, hi in stream_bounds(A.size, leaf_len)], k)

@@ -279,3 +279,77 @@ def pss_query_host(A_host: torch.Tensor, k: int, P: int, d_A: torch.Tensor | Non
         ln = int(ol[0].item())
         return oi[:ln], oc[:ln]
     return out
+
+
+# ---- on-line ingestion (include/pss.h: pss_stream_*) ---------------------------------------
+class _Stream(ctypes.Structure):
+    _fields_ = [("key_type", ctypes.c_int32), ("k", ctypes.c_uint32), ("leaf_len", ctypes.c_uint32),
+                ("batch_leaves", ctypes.c_uint32), ("n_seen", ctypes.c_uint64),
+                ("d_ws", ctypes.c_void_p), ("ws_bytes", ctypes.c_size_t)]
+
+
+_STP = ctypes.POINTER(_Stream)
+_lib.pss_stream_workspace_bytes.argtypes = [_i32, _u32, _u32, _u32]
+_lib.pss_stream_workspace_bytes.restype = _sz
+_lib.pss_stream_init.argtypes = [_STP, _i32, _u32, _u32, _u32, _vp, _sz]
+_lib.pss_stream_feed.argtypes = [_STP, _vp, _u64, _vp]
+_lib.pss_stream_feed_host.argtypes = [_STP, _vp, _u64, _vp]
+_lib.pss_stream_root.argtypes = [_STP, _SP, _vp]
+for _f in ("pss_stream_init", "pss_stream_feed", "pss_stream_feed_host", "pss_stream_root"):
+    getattr(_lib, _f).restype = _i32
+EXPORTED_SYMBOLS += ["pss_stream_workspace_bytes", "pss_stream_init", "pss_stream_feed",
+                     "pss_stream_feed_host", "pss_stream_root"]
+__all__ += ["Stream", "pss_stream_workspace_bytes"]
+
+
+def pss_stream_workspace_bytes(key_type: int, k: int, leaf_len: int, batch_leaves: int) -> int:
+    return int(_lib.pss_stream_workspace_bytes(key_type, k, leaf_len, batch_leaves))
+
+
+class Stream:
+    """On-line Space Saving over a stream fed in pieces (pss_stream_*): leaves of `leaf_len`
+    items, summary = the fixed binary COMBINE tree over the leaves so far (include/pss.h)."""
+
+    def __init__(self, k: int, leaf_len: int, key_type: int = KEY_U32, batch_leaves: int = 1024,
+                 device="cuda"):
+        nb = pss_stream_workspace_bytes(key_type, k, leaf_len, batch_leaves)
+        if nb == 0:
+            raise PssError("pss_stream_workspace_bytes", 1)
+        self.ws = torch.empty((nb,), dtype=torch.uint8, device=device)
+        self._st = _Stream()
+        _check("pss_stream_init", _lib.pss_stream_init(ctypes.byref(self._st), key_type, k, leaf_len,
+                                                       batch_leaves, self.ws.data_ptr(), nb))
+
+    @property
+    def n_seen(self) -> int:
+        return int(self._st.n_seen)
+
+    @property
+    def k(self) -> int:
+        return int(self._st.k)
+
+    @property
+    def key_type(self) -> int:
+        return int(self._st.key_type)
+
+    def _check_keys(self, chunk: torch.Tensor):
+        if _key_type(chunk) != self.key_type:
+            raise TypeError("chunk key type differs from the stream's")
+        if not chunk.is_contiguous():
+            raise ValueError("chunk must be contiguous")
+
+    def feed(self, chunk: torch.Tensor, stream=None) -> "Stream":
+        """Append a DEVICE or HOST (pinned recommended) tensor of keys."""
+        self._check_keys(chunk)
+        fn = _lib.pss_stream_feed if chunk.is_cuda else _lib.pss_stream_feed_host
+        _check("pss_stream_feed", fn(ctypes.byref(self._st), chunk.data_ptr() if chunk.numel() else None,
+                                     chunk.numel(), _stream(stream)))
+        return self
+
+    def root(self, out: Summaries | None = None, stream=None) -> Summaries:
+        """The summary of the stream so far, canonical order (one summary)."""
+        out = out or Summaries.empty(1, self.k, self.key_type, self.ws.device)
+        c = out._c()
+        _check("pss_stream_root", _lib.pss_stream_root(ctypes.byref(self._st), ctypes.byref(c),
+                                                       _stream(stream)))
+        return out

@@ -1,0 +1,316 @@
+// stream.cu -- on-line ingestion: the
+// stream is cut into consecutive leaves of `leaf_len` items (the last one possibly shorter) and
+// its summary at any point is the fixed binary COMBINE tree (reading R6) over the
+// leaves so far. Nothing is re-read: this is the on-line setting of PAPER.md:42 (no verification
+// pass; candidates come from pss_prune on the root).
+//
+// The tree is built incrementally as a binary counter. With c complete leaves, stack level j holds
+// the root of the complete subtree over leaves [p, p + 2^j) for every set bit j of c (p = the
+// higher set bits of c) -- exactly a node of the R6 tree. A feed summarizes its whole leaves with
+// K1 in batches, cuts each batch into maximal aligned power-of-two blocks, reduces every block
+// with the tree kernel (the R6 tree of 2^j leaves is the complete tree), and pushes the block
+// root with carries: a pushed node at level j whose sibling is on the stack is combined with it
+// (COMBINE, Alg. 2) into level j + 1. The summary of the stream is the right fold
+// COMBINE(S_1, COMBINE(S_2, ... COMBINE(S_t, partial))) over the stack from the highest level
+// down, then the summary of the partial leaf: this is the R6 tree over all the leaves (R6's root
+// splits off its largest complete left subtree, recursively).
+//
+// Host code only: the kernels are K1 (summarize.cu) and K2 (merge.cu).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pss {
+
+namespace {
+
+struct StreamLayout {
+  size_t stk_items, stk_counts, stk_errs, stk_sizes;  // STACK_LEVELS summaries
+  size_t tmp_items, tmp_counts, tmp_errs, tmp_sizes;  // 3 summaries: block root, carry ping-pong
+  size_t b_items, b_counts, b_errs, b_sizes;          // batch_leaves leaf summaries
+  size_t staging;                                     // leaf_len keys: the partial leaf
+  size_t hostbuf;                                     // 2 x batch_leaves * leaf_len keys (feed_host)
+  size_t scratch, total;
+};
+constexpr uint32_t STACK_LEVELS = 64;
+
+StreamLayout stream_layout(int kb, uint32_t k, uint32_t leaf_len, uint32_t batch,
+                           const DevInfo& d) {
+  StreamLayout L;
+  Bump b;
+  L.stk_items = b.take<unsigned char>((size_t)STACK_LEVELS * k * kb);
+  L.stk_counts = b.take<uint32_t>((size_t)STACK_LEVELS * k);
+  L.stk_errs = b.take<uint32_t>((size_t)STACK_LEVELS * k);
+  L.stk_sizes = b.take<uint32_t>(STACK_LEVELS);
+  L.tmp_items = b.take<unsigned char>((size_t)3 * k * kb);
+  L.tmp_counts = b.take<uint32_t>((size_t)3 * k);
+  L.tmp_errs = b.take<uint32_t>((size_t)3 * k);
+  L.tmp_sizes = b.take<uint32_t>(3);
+  L.b_items = b.take<unsigned char>((size_t)batch * k * kb);
+  L.b_counts = b.take<uint32_t>((size_t)batch * k);
+  L.b_errs = b.take<uint32_t>((size_t)batch * k);
+  L.b_sizes = b.take<uint32_t>(batch);
+  L.staging = b.take<unsigned char>((size_t)leaf_len * kb);
+  L.hostbuf = b.take<unsigned char>((size_t)2 * batch * leaf_len * kb);
+  const uint64_t nb = (uint64_t)batch * leaf_len;
+  const size_t sc = std::max({summarize_ws(nb, kb, k, batch, d), summarize_ws(leaf_len, kb, k, 1, d),
+                              merge_ws(kb, k, batch, d), combine_ws(kb, k, 1, d)});
+  L.scratch = b.take<unsigned char>(sc);
+  L.total = b.bytes();
+  return L;
+}
+
+// a view of one summary inside a workspace region of `cap` summaries
+struct One {
+  void* items;
+  uint32_t* counts;
+  uint32_t* errs;
+  uint32_t* sizes;
+};
+
+struct StreamCtx {
+  int kb;
+  uint32_t k, leaf_len, batch;
+  unsigned char* w;
+  StreamLayout L;
+  DevInfo d;
+
+  One region(size_t oi, size_t oc, size_t oe, size_t os, uint32_t i) const {
+    return One{w + oi + (size_t)i * k * kb, reinterpret_cast<uint32_t*>(w + oc) + (size_t)i * k,
+               reinterpret_cast<uint32_t*>(w + oe) + (size_t)i * k,
+               reinterpret_cast<uint32_t*>(w + os) + i};
+  }
+  One stack(uint32_t j) const { return region(L.stk_items, L.stk_counts, L.stk_errs, L.stk_sizes, j); }
+  One tmp(uint32_t i) const { return region(L.tmp_items, L.tmp_counts, L.tmp_errs, L.tmp_sizes, i); }
+  One leaf(uint32_t i) const { return region(L.b_items, L.b_counts, L.b_errs, L.b_sizes, i); }
+  void* scratch() const { return w + L.scratch; }
+
+  // the R6 root of `cnt` consecutive summaries starting at `first` (cnt = 1: canonical copy)
+  cudaError_t tree(const One& first, uint32_t cnt, const One& out, cudaStream_t s) const {
+    return merge_tree_launch(kb, k, cnt, first.items, first.counts, first.errs, first.sizes,
+                             out.items, out.counts, out.errs, out.sizes, scratch(), s, d);
+  }
+  cudaError_t combine(const One& a, const One& b, const One& out, cudaStream_t s) const {
+    return combine_launch(kb, k, 1, a.items, a.counts, a.errs, a.sizes, b.items, b.counts, b.errs,
+                          b.sizes, out.items, out.counts, out.errs, out.sizes, scratch(), s, d);
+  }
+  cudaError_t summarize(const void* A, uint64_t n, uint32_t P, const One& out,
+                        cudaStream_t s) const {
+    return summarize_launch(A, n, kb, k, P, out.items, out.counts, out.errs, out.sizes, scratch(),
+                            s, d);
+  }
+
+  // push the root of the aligned block [p, p + 2^j) of complete leaves, whose 2^j leaf summaries
+  // start at `first`; c = p is the number of complete leaves before the block
+  cudaError_t push_block(uint64_t p, uint32_t j, const One& first, cudaStream_t s) const {
+    uint32_t top = j;  // carries run while the sibling (bit `top` of p) is on the stack
+    while (top < STACK_LEVELS && ((p >> top) & 1u)) ++top;
+    if (top >= STACK_LEVELS) return cudaErrorInvalidValue;
+    if (top == j) return tree(first, 1u << j, stack(j), s);
+    cudaError_t e = tree(first, 1u << j, tmp(0), s);
+    uint32_t cur = 0;
+    for (uint32_t t = j; t < top && e == cudaSuccess; ++t) {
+      const One out = (t + 1 == top) ? stack(top) : tmp(cur == 1 ? 2 : 1);
+      e = combine(stack(t), tmp(cur), out, s);
+      cur = cur == 1 ? 2 : 1;
+    }
+    return e;
+  }
+
+  // summarize and push `nl` complete leaves read from A (nl <= batch), the first being leaf c
+  cudaError_t push_leaves(const void* A, uint64_t c, uint32_t nl, cudaStream_t s) const {
+    if (!nl) return cudaSuccess;
+    cudaError_t e = summarize(A, (uint64_t)nl * leaf_len, nl, leaf(0), s);
+    uint32_t i = 0;
+    while (i < nl && e == cudaSuccess) {
+      const uint64_t p = c + i;
+      uint32_t j = 0;  // largest aligned power-of-two block starting at p that fits
+      while (j < 31 && ((p >> j) & 1u) == 0 && i + (2u << j) <= nl) ++j;
+      e = push_block(p, j, leaf(i), s);
+      i += 1u << j;
+    }
+    return e;
+  }
+};
+
+bool ctx_of(const pss_stream* st, StreamCtx& c) {
+  c.kb = st->key_type == PSS_KEY_U32 ? 4 : (st->key_type == PSS_KEY_U64 ? 8 : 0);
+  if (!c.kb || st->k < 2 || st->k > PSS_MAX_K || st->leaf_len == 0 || st->batch_leaves == 0 ||
+      !st->d_ws)
+    return false;
+  c.k = st->k;
+  c.leaf_len = st->leaf_len;
+  c.batch = st->batch_leaves;
+  c.w = static_cast<unsigned char*>(st->d_ws);
+  c.d = dev_info();
+  c.L = stream_layout(c.kb, c.k, c.leaf_len, c.batch, c.d);
+  return st->ws_bytes >= c.L.total;
+}
+
+// f_hat <= N + floor(N/k) must fit the u32 counters (R9, invariant I of SURVEY.md 8(c))
+uint64_t stream_max_n(uint32_t k) {
+  const uint64_t lim = 0xffffffffull;
+  return lim * k / (k + 1);
+}
+
+// ingest len keys at d_chunk (device) into the stream described by c and st->n_seen
+cudaError_t feed_device(const StreamCtx& c, pss_stream* st, const void* d_chunk, uint64_t len,
+                        cudaStream_t s) {
+  const unsigned char* A = static_cast<const unsigned char*>(d_chunk);
+  const uint64_t LL = c.leaf_len;
+  uint64_t n0 = st->n_seen;
+  cudaError_t e = cudaSuccess;
+  // 1. complete the partial leaf in the staging buffer
+  const uint64_t have = n0 % LL;
+  if (have && len) {
+    const uint64_t t = std::min(len, LL - have);
+    e = cudaMemcpyAsync(c.w + c.L.staging + have * c.kb, A, t * c.kb, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && have + t == LL) e = c.push_leaves(c.w + c.L.staging, n0 / LL, 1, s);
+    if (e != cudaSuccess) return e;
+    A += t * c.kb;
+    len -= t;
+    n0 += t;
+  }
+  // 2. whole leaves straight from the chunk, in batches of the leaf buffer's capacity
+  uint64_t whole = len / LL;
+  while (whole && e == cudaSuccess) {
+    const uint32_t nl = (uint32_t)std::min<uint64_t>(whole, c.batch);
+    e = c.push_leaves(A, n0 / LL, nl, s);
+    A += (uint64_t)nl * LL * c.kb;
+    len -= (uint64_t)nl * LL;
+    n0 += (uint64_t)nl * LL;
+    whole -= nl;
+  }
+  // 3. the rest starts a new partial leaf
+  if (len && e == cudaSuccess)
+    e = cudaMemcpyAsync(c.w + c.L.staging, A, len * c.kb, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) st->n_seen = n0 + len;
+  return e;
+}
+
+}  // namespace
+}  // namespace pss
+
+using namespace pss;
+
+extern "C" {
+
+size_t pss_stream_workspace_bytes(pss_key_type kt, uint32_t k, uint32_t leaf_len,
+                                  uint32_t batch_leaves) {
+  const int kb = kt == PSS_KEY_U32 ? 4 : (kt == PSS_KEY_U64 ? 8 : 0);
+  if (!kb || k < 2 || leaf_len == 0 || batch_leaves == 0) return 0;
+  return stream_layout(kb, k, leaf_len, batch_leaves, dev_info()).total;
+}
+
+pss_status pss_stream_init(pss_stream* st, pss_key_type kt, uint32_t k, uint32_t leaf_len,
+                           uint32_t batch_leaves, void* d_ws, size_t ws_bytes) {
+  if (!st || !d_ws || k < 2 || leaf_len == 0 || batch_leaves == 0 ||
+      (kt != PSS_KEY_U32 && kt != PSS_KEY_U64))
+    return PSS_ERR_INVALID_ARG;
+  if (k > PSS_MAX_K || leaf_len > PSS_MAX_N || (uint64_t)batch_leaves * leaf_len > PSS_MAX_N)
+    return PSS_ERR_UNSUPPORTED;
+  pss_stream s0;
+  s0.key_type = kt;
+  s0.k = k;
+  s0.leaf_len = leaf_len;
+  s0.batch_leaves = batch_leaves;
+  s0.n_seen = 0;
+  s0.d_ws = d_ws;
+  s0.ws_bytes = ws_bytes;
+  StreamCtx c;
+  if (!ctx_of(&s0, c)) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  *st = s0;
+  return PSS_OK;
+}
+
+pss_status pss_stream_feed(pss_stream* st, const void* d_chunk, uint64_t len,
+                           cudaStream_t stream) {
+  if (!st || (len && !d_chunk)) return PSS_ERR_INVALID_ARG;
+  StreamCtx c;
+  if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
+  if (st->n_seen + len > stream_max_n(st->k) || st->n_seen + len < st->n_seen)
+    return PSS_ERR_UNSUPPORTED;
+  return feed_device(c, st, d_chunk, len, stream) == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
+}
+
+pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t len,
+                                cudaStream_t stream) {
+  if (!st || (len && !h_chunk)) return PSS_ERR_INVALID_ARG;
+  StreamCtx c;
+  if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
+  if (st->n_seen + len > stream_max_n(st->k) || st->n_seen + len < st->n_seen)
+    return PSS_ERR_UNSUPPORTED;
+  if (!len) return PSS_OK;
+  // pieces of one batch of leaves, copied on a private stream into two alternating device
+  // buffers; piece g is ingested on `stream` as soon as it has landed, and buffer g % 2 is
+  // refilled only after the ingestion of piece g - 2 is done with it
+  const uint64_t piece = (uint64_t)c.batch * c.leaf_len;
+  unsigned char* buf[2] = {c.w + c.L.hostbuf, c.w + c.L.hostbuf + piece * c.kb};
+  cudaStream_t cs = nullptr;
+  cudaEvent_t landed[2] = {}, used[2] = {};
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming);
+    // the buffers are free once the work already enqueued on `stream` is done
+    if (e == cudaSuccess) e = cudaEventRecord(used[i], stream);
+  }
+  const unsigned char* h = static_cast<const unsigned char*>(h_chunk);
+  for (uint64_t off = 0, g = 0; off < len && e == cudaSuccess; off += piece, ++g) {
+    const uint64_t m = std::min(piece, len - off);
+    const int b = (int)(g & 1);
+    e = cudaStreamWaitEvent(cs, used[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(buf[b], h + off * c.kb, m * c.kb, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(landed[b], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, landed[b], 0);
+    if (e == cudaSuccess) e = feed_device(c, st, buf[b], m, stream);
+    if (e == cudaSuccess) e = cudaEventRecord(used[b], stream);
+  }
+  // the copy stream's last copy precedes work on `stream` (waited above); release is
+  // stream-ordered
+  for (int i = 0; i < 2; ++i) {
+    if (landed[i]) cudaEventDestroy(landed[i]);
+    if (used[i]) cudaEventDestroy(used[i]);
+  }
+  if (cs) cudaStreamDestroy(cs);
+  return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
+}
+
+pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream_t stream) {
+  if (!st || !root || !root->items || !root->counts || !root->errs || !root->sizes)
+    return PSS_ERR_INVALID_ARG;
+  StreamCtx c;
+  if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
+  if (root->k != st->k || root->key_type != st->key_type || root->count != 1)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const One out{root->items, root->counts, root->errs, root->sizes};
+  const uint64_t complete = st->n_seen / st->leaf_len, have = st->n_seen % st->leaf_len;
+  // the fold's operands from the right: the partial leaf, then stack levels upwards
+  One ops[STACK_LEVELS + 1];
+  uint32_t nops = 0;
+  cudaError_t e = cudaSuccess;
+  if (have) {
+    ops[nops++] = c.leaf(0);
+    e = c.summarize(c.w + c.L.staging, have, 1, c.leaf(0), stream);
+  }
+  for (uint32_t j = 0; j < 64; ++j)
+    if ((complete >> j) & 1u) ops[nops++] = c.stack(j);
+  if (e != cudaSuccess) return PSS_ERR_CUDA;
+  if (nops == 0) return cudaMemsetAsync(root->sizes, 0, sizeof(uint32_t), stream) == cudaSuccess
+                            ? PSS_OK
+                            : PSS_ERR_CUDA;
+  if (nops == 1) return c.tree(ops[0], 1, out, stream) == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
+  // acc = ops[0]; acc = COMBINE(ops[i], acc) for i = 1..nops-1, the last one into `root`
+  One acc = ops[0];
+  uint32_t cur = 1;
+  for (uint32_t i = 1; i < nops && e == cudaSuccess; ++i) {
+    const One dst = (i + 1 == nops) ? out : c.tmp(cur);
+    e = c.combine(ops[i], acc, dst, stream);
+    acc = dst;
+    cur = cur == 1 ? 2 : 1;
+  }
+  return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
+}
+
+}  // extern "C"

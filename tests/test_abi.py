@@ -123,3 +123,35 @@ def test_product_path_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"\boracle\b", src.replace("oracle/", "")), f
+
+
+def test_stream_validation_before_launch(pss):
+    """pss_stream_*: bad arguments return status codes; init launches nothing (include/pss.h)."""
+    lib = pss._lib
+    st = pss._Stream()
+    by = ctypes.byref
+    dummy = ctypes.c_void_p(0x1000)
+    nb = pss.pss_stream_workspace_bytes(pss.KEY_U32, 1000, 65536, 16)
+    assert nb > 16 * 65536 * 4 * 2 and pss.pss_stream_workspace_bytes(pss.KEY_U32, 1, 10, 1) == 0
+    assert pss.pss_stream_workspace_bytes(7, 10, 10, 1) == 0
+    assert lib.pss_stream_init(None, 0, 10, 100, 4, dummy, 1 << 30) == 1
+    assert lib.pss_stream_init(by(st), 0, 1, 100, 4, dummy, 1 << 30) == 1       # k < 2
+    assert lib.pss_stream_init(by(st), 0, 10, 0, 4, dummy, 1 << 30) == 1        # leaf_len 0
+    assert lib.pss_stream_init(by(st), 0, 10, 100, 0, dummy, 1 << 30) == 1      # batch 0
+    assert lib.pss_stream_init(by(st), 3, 10, 100, 4, dummy, 1 << 30) == 1      # key type
+    assert lib.pss_stream_init(by(st), 0, 70000, 100, 4, dummy, 1 << 30) == 2   # k > PSS_MAX_K
+    assert lib.pss_stream_init(by(st), 0, 10, 1 << 20, 1 << 12, dummy, 1 << 40) == 2  # batch > 2^31
+    assert lib.pss_stream_init(by(st), 0, 10, 100, 4, dummy, 1024) == 4         # workspace
+    need = pss.pss_stream_workspace_bytes(pss.KEY_U32, 10, 100, 4)
+    assert lib.pss_stream_init(by(st), 0, 10, 100, 4, dummy, need) == 0
+    assert (st.k, st.leaf_len, st.batch_leaves, st.n_seen) == (10, 100, 4, 0)
+    # feeds: null chunk with len > 0; a stream longer than the u32 counters allow (R9)
+    assert lib.pss_stream_feed(by(st), None, 5, None) == 1
+    assert lib.pss_stream_feed(by(st), dummy, 1 << 32, None) == 2
+    assert lib.pss_stream_feed_host(by(st), dummy, (1 << 32) - 1, None) == 2
+    assert st.n_seen == 0
+    # root: capacity mismatch
+    root = pss._Summ(0, 11, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_stream_root(by(st), by(root), None) == 3
+    root = pss._Summ(1, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_stream_root(by(st), by(root), None) == 3

@@ -287,3 +287,43 @@ def test_root_guarantees_at_scale():
         assert f.get(x, 0) <= cc <= f.get(x, 0) + e and e <= n // k
     for x in u[c * k > n].tolist():
         assert x in set(root.items.tolist())
+
+
+# ---------------------------------------------------------------- f2: on-line stream (R14)
+def test_stream_golden(golden):
+    """Hand-derived streams E7/E8 (cut into fixed-length leaves, R6 tree over them)."""
+    for case in golden["stream"]:
+        A = letters(case["stream"])
+        k, ll = case["k"], case["leaf_len"]
+        lv = [oracle.space_saving(A, k, lo, hi).as_tuples() for lo, hi in oracle.stream_bounds(A.size, ll)]
+        assert lv == [S(x) for x in case["leaves"]], case["name"]
+        assert oracle.stream_root(A, k, ll).as_tuples() == S(case["root"]), case["name"]
+
+
+def test_stream_special_cases():
+    """leaf_len >= n: one leaf, i.e. sequential SS in canonical order; n = P * leaf_len: exactly
+    Algorithm 1's blocks (P:92-95 give r * leaf_len); empty stream: empty summary."""
+    import inputs
+    A = inputs.zipf(5000, 1.1, 300, seed=3)
+    u, c = np.unique(A, return_counts=True)
+    order = np.lexsort((u, -c.astype(np.int64)))
+    # k >= distinct: the single leaf is the exact histogram (textbook unique)
+    assert oracle.stream_root(A, 400, 10_000).as_tuples() == [(int(u[i]), int(c[i]), 0) for i in order]
+    for ll in (625, 1000, 5000):
+        assert oracle.stream_bounds(A.size, ll) == oracle.bounds(A.size, A.size // ll)
+    assert oracle.stream_bounds(10, 4) == [(0, 4), (4, 8), (8, 10)]
+    assert len(oracle.stream_root(A[:0], 10, 7)) == 0
+
+
+@pytest.mark.parametrize("n,ll,k", [(9999, 700, 20), (20000, 1024, 50), (4097, 13, 5)])
+def test_stream_guarantees(n, ll, k):
+    """The paper's guarantees hold for the on-line summary of a ragged stream (exact counts from
+    np.unique): f <= f_hat <= f + err, err <= n/k, sum of counts <= n, every f > n/k reported."""
+    import inputs
+    A = inputs.zipf(n, 1.1, 1e5, seed=n)
+    R = oracle.stream_root(A, k, ll)
+    f = hist(A)
+    assert int(R.counts.sum()) <= n and len(R) <= k
+    for x, cc, e in R.as_tuples():
+        assert f.get(x, 0) <= cc <= f.get(x, 0) + e and e <= n // k
+    assert {x for x, v in f.items() if v * k > n} <= set(R.items.tolist())
