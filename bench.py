@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true",
                     help="profiling runs only: skip the end-to-end leg (e2e is then null)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--no-stream", action="store_true", help="skip the on-line stream leg (f2)")
+    ap.add_argument("--stream-passes", type=int, default=4,
+                    help="stream leg: the workload's array fed this many times (one stream)")
     return ap.parse_args()
 
 
@@ -200,6 +203,56 @@ def config_of(w, P, gpus):
     return d
 
 
+# ------------------------------------------------------------------------------ stream leg (f2)
+def stream_leg(pss, w, P, h_A, d_A, passes, dev):
+    """On-line ingestion (pss_stream_*): one stream of passes * n keys (the
+    workload's array fed `passes` times), leaves of n/P keys, then its root and the on-line
+    candidates (pss_prune; no verification pass in the on-line setting). Timed with CUDA events on
+    the stream, once from device memory (K1 + incremental merges) and once from pinned host memory
+    (pieces of batch_leaves leaves copied on a private stream, overlapped with the kernels); the
+    host leg is bound by the host->device link, measured here with a plain pinned copy."""
+    import torch
+    n, kb = w.n, w.key_bytes
+    kt = pss.KEY_U32 if kb == 4 else pss.KEY_U64
+    st_dev = torch.cuda.current_stream()
+    out = {}
+    for src_name, src in (("device", d_A), ("host", h_A)):
+        ts = []
+        for rep in range(2):  # the first run warms up
+            st = pss.Stream(w.k, n // P, kt, batch_leaves=P)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(st_dev)
+            for _ in range(passes):
+                st.feed(src)
+            root = st.root()
+            cand, n_cand = pss.pss_prune(root, st.n_seen)
+            b.record(st_dev)
+            torch.cuda.synchronize()
+            if rep:
+                ts.append(a.elapsed_time(b))
+            del st
+        ms = min(ts)
+        out[src_name] = {"value": round(passes * n / (ms * 1e-3) / 1e9, 3), "unit": "Gitems/s",
+                         "ms": round(ms, 3), "n_cand": int(n_cand.item())}
+    # the link's own bandwidth: one pinned host -> device copy of the same bytes
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st_dev)
+    d_A.copy_(h_A, non_blocking=True)
+    b.record(st_dev)
+    torch.cuda.synchronize()
+    h2d = n * kb / (a.elapsed_time(b) * 1e-3) / 1e9
+    host_gbs = passes * n * kb / (out["host"]["ms"] * 1e-3) / 1e9
+    out["host"]["roofline"] = {"bound": "h2d", "achieved": round(host_gbs, 2),
+                               "peak": round(h2d, 2), "unit": "GB/s",
+                               "frac": round(host_gbs / h2d, 4),
+                               "peak_source": "pinned torch copy of the same bytes, this run"}
+    out["items"] = passes * n
+    out["leaf_len"] = n // P
+    out["batch_leaves"] = P
+    return out
+
+
 # ------------------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -333,6 +386,8 @@ def main():
             "gpu_launches": runner.launches_per_step * K,
             "clocks": clk.summary(),
             "result_len": ln}
+    if world == 1 and not args.no_stream:
+        line["stream"] = stream_leg(pss, w, P, h_A, d_A, args.stream_passes, dev)
     if world == 1 and not args.no_cpu_baseline:
         rate, desc, cores, dt = oracle_sample(w, args.cpu_seconds, host_threads(), h_A.numpy())
         line["cpu_baseline"] = {"value": round(rate / 1e9, 6), "unit": "Gitems/s", "cores": cores,
