@@ -53,7 +53,8 @@ typedef enum {
   PSS_OP_MERGE = 1,
   PSS_OP_COMBINE = 2,
   PSS_OP_VERIFY = 3,
-  PSS_OP_QUERY = 4
+  PSS_OP_QUERY = 4,
+  PSS_OP_EXACT = 5 /* pss_exact_kmajority; P is ignored */
 } pss_op;
 
 #define PSS_MAX_K 65000u
@@ -228,6 +229,49 @@ pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t le
 /* The summary of the stream so far (the R6 tree over its leaves, the partial leaf included), in
  * canonical order (R5) into root (count 1, same k and key type). Does not change the stream. */
 pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream_t stream);
+
+/*
+ * ---- Accuracy ---------------------------------------------
+ * pss_exact_kmajority -- the k-majority set {(x, f(x)) : f(x) >= floor(n/k) + 1}
+ * computed WITHOUT Space Saving, as the truth for recall and precision: A is cut into
+ * sub-blocks of 4096 keys; an item with f(x) > n/k has f_r(x) > L_r/k in some sub-block r, so the
+ * locally heavy keys of every sub-block (exact per-sub-block histograms) form a candidate set that
+ * a second pass counts exactly. Output ordered by (f desc, x asc), like pss_query.
+ *   d_out_items : capacity k keys; d_out_counts : capacity k uint64; d_out_len : one uint32.
+ *   d_overflow  : optional (may be NULL) uint32 set to 1 if the candidate set outgrew its table
+ *                 (2^12..2^24 entries sized from n*k/4096; then the output is incomplete), else 0.
+ *   workspace   : pss_workspace_bytes(PSS_OP_EXACT, n, k, 0, kt).
+ */
+pss_status pss_exact_kmajority(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                               void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                               uint32_t* d_overflow, void* d_ws, size_t ws_bytes,
+                               cudaStream_t stream);
+
+/* The paper's accuracy metrics of Algorithm 1's output (two ARE populations). */
+typedef struct {
+  uint64_t n_reported;      /* candidates reported by Algorithm 1 (pss_prune of the root) */
+  uint64_t n_reported_true; /* of which true k-majority items (exact count >= floor(n/k) + 1) */
+  uint64_t n_true;          /* true k-majority items (pss_exact_kmajority) */
+  double precision;         /* n_reported_true / n_reported (1 if nothing is reported) */
+  double recall;            /* n_reported_true / n_true (1 if there is no k-majority item) */
+  double are_reported;      /* mean |f - f_hat| / f over the reported items (0 if none) */
+  double are_true;          /* mean over the true k-majority items; an unreported one counts 1 */
+} pss_accuracy_report;
+
+/*
+ * pss_accuracy -- writes *d_report (device memory) for the candidates of `root`:
+ *   root     : the root summary (canonical order, as written by pss_merge / pss_stream_root); the
+ *              reported items are its first *d_n_cand counters, their estimates f_hat its counts.
+ *   n        : the stream length the root summarizes.
+ *   d_n_cand : device uint32 written by pss_prune(root, n, ...).
+ *   d_exact  : device uint64[*d_n_cand]: pss_verify of those candidates (exact f).
+ *   d_n_true : device uint32, the length written by pss_exact_kmajority (or any exact count of
+ *              the items with f >= floor(n/k) + 1).
+ * ARE sums are fp64 in a fixed order (deterministic).
+ */
+pss_status pss_accuracy(const pss_summaries* root, uint64_t n, const uint32_t* d_n_cand,
+                        const uint64_t* d_exact, const uint32_t* d_n_true,
+                        pss_accuracy_report* d_report, cudaStream_t stream);
 
 /* Human-readable name of a status. */
 const char* pss_status_string(pss_status s);

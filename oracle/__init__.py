@@ -239,3 +239,33 @@ def stream_root(A, k: int, leaf_len: int) -> Summary:
     if A.size == 0:
         return empty_summary()
     return tree([space_saving(A, k, lo, hi) for lo, hi in stream_bounds(A.size, leaf_len)], k)
+
+
+def kmajority(A, k: int) -> tuple[np.ndarray, np.ndarray]:
+    """The k-majority set by its plain definition {(x, f(x)) : f(x) > n/k}
+    from a sort-based exact histogram (np.unique), ordered (f desc, x asc)."""
+    A, _ = _keys(A)
+    u, c = np.unique(A, return_counts=True)
+    sel = c.astype(np.uint64) * np.uint64(k) > np.uint64(A.size)
+    u, c = u[sel].astype(np.uint64), c[sel].astype(np.uint64)
+    order = np.lexsort((u, -c.astype(np.int64)))
+    return u[order], c[order]
+
+
+def accuracy(reported, fhat, truth: dict, n: int, k: int) -> dict:
+    """The paper's accuracy metrics with SPEC's conventions:
+    reported items with estimates f_hat; truth = exact frequencies {x: f(x)}. precision =
+    |reported & T| / |reported| (1 if nothing is reported), recall = |reported & T| / |T| (1 if T
+    is empty), relative error |f - f_hat| / f averaged over the reported items (ARE, 0 if none)
+    and over T (an unreported true item counts 1)."""
+    thr = n // k + 1
+    T = {x for x, f in truth.items() if f >= thr}
+    rep = [int(x) for x in reported]
+    est = dict(zip(rep, [int(v) for v in fhat]))
+    hit = [x for x in rep if x in T]
+    rel = {x: abs(truth[x] - est[x]) / truth[x] for x in rep}
+    return {"n_reported": len(rep), "n_reported_true": len(hit), "n_true": len(T),
+            "precision": len(hit) / len(rep) if rep else 1.0,
+            "recall": len(hit) / len(T) if T else 1.0,
+            "are_reported": float(np.mean([rel[x] for x in rep])) if rep else 0.0,
+            "are_true": float(np.mean([rel[x] if x in est else 1.0 for x in T])) if T else 0.0}

@@ -353,3 +353,52 @@ class Stream:
         _check("pss_stream_root", _lib.pss_stream_root(ctypes.byref(self._st), ctypes.byref(c),
                                                        _stream(stream)))
         return out
+
+
+# ---- accuracy (include/pss.h: pss_exact_kmajority, pss_accuracy) ----------------------------
+OP_EXACT = 5
+
+
+class AccuracyReport(ctypes.Structure):
+    _fields_ = [("n_reported", ctypes.c_uint64), ("n_reported_true", ctypes.c_uint64),
+                ("n_true", ctypes.c_uint64), ("precision", ctypes.c_double),
+                ("recall", ctypes.c_double), ("are_reported", ctypes.c_double),
+                ("are_true", ctypes.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib.pss_exact_kmajority.argtypes = [_vp, _u64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+_lib.pss_exact_kmajority.restype = _i32
+_lib.pss_accuracy.argtypes = [_SP, _u64, _vp, _vp, _vp, _vp, _vp]
+_lib.pss_accuracy.restype = _i32
+EXPORTED_SYMBOLS += ["pss_exact_kmajority", "pss_accuracy"]
+__all__ += ["OP_EXACT", "AccuracyReport", "pss_exact_kmajority", "pss_accuracy"]
+
+
+def pss_exact_kmajority(A: torch.Tensor, k: int, workspace: torch.Tensor | None = None,
+                        stream=None):
+    """The k-majority set of A computed without Space Saving (local heavy hitters + exact counts):
+    (items[k], counts[k] uint64, length[1], overflow[1]) device tensors, (f desc, x asc)."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    items = torch.empty((k,), dtype=_key_dtype(kt), device=A.device)
+    counts = torch.empty((k,), dtype=torch.uint64, device=A.device)
+    length = torch.zeros((1,), dtype=torch.uint32, device=A.device)
+    overflow = torch.zeros((1,), dtype=torch.uint32, device=A.device)
+    ws = _ws(pss_workspace_bytes(OP_EXACT, A.numel(), k, 0, kt), workspace, A.device)
+    _check("pss_exact_kmajority", _lib.pss_exact_kmajority(
+        A.data_ptr(), A.numel(), kt, k, items.data_ptr(), counts.data_ptr(), length.data_ptr(),
+        overflow.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return items, counts, length, overflow
+
+
+def pss_accuracy(root: Summaries, n: int, n_cand: torch.Tensor, exact: torch.Tensor,
+                 n_true: torch.Tensor, stream=None) -> AccuracyReport:
+    """Precision, recall and ARE of the root's pruned candidates (synchronises)."""
+    out = torch.zeros((ctypes.sizeof(AccuracyReport),), dtype=torch.uint8, device=root.items.device)
+    c = root._c()
+    _check("pss_accuracy", _lib.pss_accuracy(ctypes.byref(c), n, n_cand.data_ptr(), exact.data_ptr(),
+                                             n_true.data_ptr(), out.data_ptr(), _stream(stream)))
+    return AccuracyReport.from_buffer_copy(bytes(out.cpu().numpy()))

@@ -89,6 +89,7 @@ size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_t
     case PSS_OP_COMBINE: return combine_ws(kb, k, P, d);
     case PSS_OP_VERIFY: return verify_ws(kb, k, d);
     case PSS_OP_QUERY: return q_layout(n, kb, k, P ? P : 1, d).total;
+    case PSS_OP_EXACT: return exact_ws(kb, n, k);
   }
   return 0;
 }

@@ -166,6 +166,7 @@ size_t verify_ws(int kb, uint32_t cap, const DevInfo& d);
 cudaError_t verify_launch(const void* A, uint64_t n, int kb, const void* cand, uint32_t cap,
                           const uint32_t* d_n_cand, uint64_t* exact, void* ws, cudaStream_t s,
                           const DevInfo& d);
+size_t exact_ws(int kb, uint64_t n, uint32_t k);
 cudaError_t result_launch(int kb, uint32_t cap, const void* cand, const uint32_t* d_n_cand,
                           const uint64_t* exact, uint64_t n, uint32_t k, void* out_items,
                           uint64_t* out_counts, uint32_t* out_len, cudaStream_t s);

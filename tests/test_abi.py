@@ -155,3 +155,23 @@ def test_stream_validation_before_launch(pss):
     assert lib.pss_stream_root(by(st), by(root), None) == 3
     root = pss._Summ(1, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
     assert lib.pss_stream_root(by(st), by(root), None) == 3
+
+
+def test_accuracy_validation_before_launch(pss):
+    lib = pss._lib
+    dummy = ctypes.c_void_p(0x1000)
+    ws = pss.pss_workspace_bytes(pss.OP_EXACT, 1 << 29, 1000, 0, pss.KEY_U32)
+    assert ws > (1 << 24) * 4
+    assert lib.pss_exact_kmajority(dummy, 100, 0, 1, dummy, dummy, dummy, None, dummy, ws, None) == 1
+    assert lib.pss_exact_kmajority(dummy, 100, 5, 10, dummy, dummy, dummy, None, dummy, ws, None) == 1
+    assert lib.pss_exact_kmajority(dummy, 100, 0, 10, None, dummy, dummy, None, dummy, ws, None) == 1
+    assert lib.pss_exact_kmajority(dummy, (1 << 31) + 1, 0, 10, dummy, dummy, dummy, None, dummy,
+                                   1 << 40, None) == 2
+    assert lib.pss_exact_kmajority(dummy, 100, 0, 10, dummy, dummy, dummy, None, dummy, 64, None) == 4
+    root = pss._Summ(0, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    by = ctypes.byref
+    assert lib.pss_accuracy(by(root), 100, None, dummy, dummy, dummy, None) == 1
+    assert lib.pss_accuracy(by(root), 100, dummy, dummy, dummy, None, None) == 1
+    two = pss._Summ(0, 10, 2, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_accuracy(by(two), 100, dummy, dummy, dummy, dummy, None) == 1
+    assert ctypes.sizeof(pss.AccuracyReport) == 56

@@ -41,14 +41,20 @@ def run_path(pss, A, k, P):
     cand, n_cand = pss.pss_prune(root, A.size)
     exact = pss.pss_verify(dA, cand, n_cand)
     items, counts, length = pss.pss_query(dA, k, P)
+    # the same answer without Space Saving (f3's truth: local heavy hitters + exact counts)
+    x_items, x_counts, x_len, x_over = pss.pss_exact_kmajority(dA, k)
     torch.cuda.synchronize()
     nc = int(n_cand.item())
     ln = int(length.item())
+    xl = int(x_len.item())
+    assert int(x_over.item()) == 0
     return dict(leaves=leaves, root=root,
                 cand=cand[:nc].cpu().numpy().astype(np.uint64).tolist(),
                 exact=exact[:nc].cpu().numpy().astype(np.uint64).tolist(),
                 result=(items[:ln].cpu().numpy().astype(np.uint64).tolist(),
-                        counts[:ln].cpu().numpy().astype(np.uint64).tolist()))
+                        counts[:ln].cpu().numpy().astype(np.uint64).tolist()),
+                exact_km=(x_items[:xl].cpu().numpy().astype(np.uint64).tolist(),
+                          x_counts[:xl].cpu().numpy().astype(np.uint64).tolist()))
 
 
 def assert_full_parity(pss, A, k, P, threads=8):
@@ -61,6 +67,7 @@ def assert_full_parity(pss, A, k, P, threads=8):
     assert got["exact"] == ref.exact.tolist()
     assert got["result"][0] == ref.result[0].tolist()
     assert got["result"][1] == ref.result[1].tolist()
+    assert got["exact_km"] == got["result"]  # == the oracle's answer, checked just above
     return got, ref
 
 
@@ -300,6 +307,7 @@ def test_full_size(pss, name):
     assert got["exact"] == oracle.verify(A, np.array(got["cand"], np.uint64)).tolist()
     want = bruteforce_kmajority(A, k)
     assert got["result"] == want
+    assert got["exact_km"] == want
     assert set(want[0]) <= set(items.tolist())  # recall 1
 
 

@@ -327,3 +327,47 @@ def test_stream_guarantees(n, ll, k):
     for x, cc, e in R.as_tuples():
         assert f.get(x, 0) <= cc <= f.get(x, 0) + e and e <= n // k
     assert {x for x, v in f.items() if v * k > n} <= set(R.items.tolist())
+
+
+# ---------------------------------------------------------------- f3: accuracy metrics
+def test_kmajority_bruteforce():
+    """The k-majority definition by counting in a plain loop on small streams."""
+    rng = np.random.default_rng(3)
+    for trial in range(40):
+        n = int(rng.integers(0, 300))
+        k = int(rng.integers(2, 12))
+        A = rng.integers(0, int(rng.integers(1, 20)), size=n).astype(np.uint32)
+        cnt = {}
+        for x in A.tolist():
+            cnt[x] = cnt.get(x, 0) + 1
+        want = sorted([(x, c) for x, c in cnt.items() if c * k > n], key=lambda t: (-t[1], t[0]))
+        u, c = oracle.kmajority(A, k)
+        assert list(zip(u.tolist(), c.tolist())) == want
+
+
+def test_accuracy_spec_examples():
+    """S:341 (reported {a,b}, T {a} -> precision 0.5, recall 1), S:347 (ARE 0), S:348 (ARE of
+    [(a,11),(b,20)] against {a:10, b:20} = mean(0.1, 0) = 0.05)."""
+    r = oracle.accuracy([1, 2], [6, 4], {1: 5, 2: 2}, n=10, k=3)  # threshold 4: T = {a}
+    assert (r["precision"], r["recall"], r["n_true"]) == (0.5, 1.0, 1)
+    r = oracle.accuracy([1], [10], {1: 10}, n=10, k=2)
+    assert r["are_reported"] == 0.0 and r["are_true"] == 0.0
+    r = oracle.accuracy([1, 2], [11, 20], {1: 10, 2: 20}, n=30, k=2)
+    assert abs(r["are_reported"] - 0.05) < 1e-15
+    # nothing reported, nothing true: SPEC's conventions (S:338-339, S:349)
+    r = oracle.accuracy([], [], {1: 1, 2: 1}, n=2, k=2)
+    assert (r["precision"], r["recall"], r["are_reported"]) == (1.0, 1.0, 0.0)
+    # a true item not reported counts relative error 1 in the T population
+    r = oracle.accuracy([2], [3], {1: 6, 2: 3}, n=9, k=3)  # threshold 4: T = {a}
+    assert (r["recall"], r["are_true"], r["precision"]) == (0.0, 1.0, 0.0)
+
+
+def test_accuracy_exact_case_is_zero():
+    """single worker with k >= distinct -> all counts exact -> ARE 0, precision 1."""
+    import inputs
+    A = inputs.zipf(3000, 1.3, 200, seed=8)
+    k = 250
+    root = oracle.tree(oracle.leaves(A, k, 1), k)
+    cand = oracle.prune(root, A.size, k)
+    r = oracle.accuracy(cand, root.counts[:cand.size], hist(A), A.size, k)
+    assert r["are_reported"] == 0.0 and r["precision"] == 1.0 and r["recall"] == 1.0
