@@ -273,6 +273,29 @@ pss_status pss_accuracy(const pss_summaries* root, uint64_t n, const uint32_t* d
                         const uint64_t* d_exact, const uint32_t* d_n_true,
                         pss_accuracy_report* d_report, cudaStream_t stream);
 
+/*
+ * ---- Hybrid decomposition ---------------------------------
+ * The paper's hybrid MPI/OpenMP design as an alternative tree shape: Pp
+ * processes take the blocks floor(p n / Pp) .. floor((p+1) n / Pp) - 1 (Alg. 1 l.3-4 at the
+ * process level) and each splits its block again among T threads with the same formulas; leaf
+ * r = p*T + t. Each process reduces its T leaves with the fixed binary tree (R6), then the Pp
+ * process roots are reduced with the same tree. Pp = 1 or T = 1 is Algorithm 1 with T or Pp
+ * blocks; with T a power of two and Pp*T dividing n it is bit for bit pss_summarize + pss_merge
+ * with P = Pp*T. COMBINE is not associative, so other shapes give other (equally guaranteed)
+ * roots.
+ */
+size_t pss_hybrid_workspace_bytes(uint64_t n, uint32_t k, uint32_t Pp, uint32_t T,
+                                  pss_key_type kt);
+/* leaves: count == Pp*T, slot order, leaf p*T + t = thread t of process p. */
+pss_status pss_summarize_hybrid(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                                uint32_t Pp, uint32_t T, pss_summaries* leaves, void* d_ws,
+                                size_t ws_bytes, cudaStream_t stream);
+/* leaves->count must be a multiple of T (Pp = count / T); root canonical (R5). Workspace:
+ * pss_hybrid_workspace_bytes(0, k, Pp, T, kt). Non-power-of-two T runs one tree launch per
+ * process. */
+pss_status pss_merge_hybrid(const pss_summaries* leaves, uint32_t T, pss_summaries* root,
+                            void* d_ws, size_t ws_bytes, cudaStream_t stream);
+
 /* Human-readable name of a status. */
 const char* pss_status_string(pss_status s);
 

@@ -269,3 +269,21 @@ def accuracy(reported, fhat, truth: dict, n: int, k: int) -> dict:
             "recall": len(hit) / len(T) if T else 1.0,
             "are_reported": float(np.mean([rel[x] for x in rep])) if rep else 0.0,
             "are_true": float(np.mean([rel[x] if x in est else 1.0 for x in T])) if T else 0.0}
+
+
+def hybrid_bounds(n: int, Pp: int, T: int) -> list[tuple[int, int]]:
+    """The hybrid decomposition: Alg. 1 l.3-4 among Pp
+    processes, then again among the T threads of each process; leaf p*T + t."""
+    out = []
+    for plo, phi in bounds(n, Pp):
+        out += [(plo + lo, plo + hi) for lo, hi in bounds(phi - plo, T)]
+    return out
+
+
+def hybrid(A, k: int, Pp: int, T: int) -> tuple[list, Summary]:
+    """Leaves of the hybrid decomposition, each process's fixed tree (R6) over its T leaves, then
+    the fixed tree over the Pp process roots."""
+    A, _ = _keys(A)
+    lv = [space_saving(A, k, lo, hi) for lo, hi in hybrid_bounds(A.size, Pp, T)]
+    roots = [tree(lv[p * T:(p + 1) * T], k) for p in range(Pp)]
+    return lv, tree(roots, k)

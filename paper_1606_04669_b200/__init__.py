@@ -402,3 +402,44 @@ def pss_accuracy(root: Summaries, n: int, n_cand: torch.Tensor, exact: torch.Ten
     _check("pss_accuracy", _lib.pss_accuracy(ctypes.byref(c), n, n_cand.data_ptr(), exact.data_ptr(),
                                              n_true.data_ptr(), out.data_ptr(), _stream(stream)))
     return AccuracyReport.from_buffer_copy(bytes(out.cpu().numpy()))
+
+
+# ---- hybrid decomposition (include/pss.h: pss_*_hybrid) ------------------------------------
+_lib.pss_hybrid_workspace_bytes.argtypes = [_u64, _u32, _u32, _u32, _i32]
+_lib.pss_hybrid_workspace_bytes.restype = _sz
+_lib.pss_summarize_hybrid.argtypes = [_vp, _u64, _i32, _u32, _u32, _u32, _SP, _vp, _sz, _vp]
+_lib.pss_summarize_hybrid.restype = _i32
+_lib.pss_merge_hybrid.argtypes = [_SP, _u32, _SP, _vp, _sz, _vp]
+_lib.pss_merge_hybrid.restype = _i32
+EXPORTED_SYMBOLS += ["pss_hybrid_workspace_bytes", "pss_summarize_hybrid", "pss_merge_hybrid"]
+__all__ += ["pss_hybrid_workspace_bytes", "pss_summarize_hybrid", "pss_merge_hybrid"]
+
+
+def pss_hybrid_workspace_bytes(n: int, k: int, Pp: int, T: int, key_type: int) -> int:
+    return int(_lib.pss_hybrid_workspace_bytes(n, k, Pp, T, key_type))
+
+
+def pss_summarize_hybrid(A: torch.Tensor, k: int, Pp: int, T: int, out: Summaries | None = None,
+                         workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """Leaves of the two-level (processes x threads) decomposition: leaf p*T + t."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    out = out or Summaries.empty(Pp * T, k, kt, A.device)
+    ws = _ws(pss_hybrid_workspace_bytes(A.numel(), k, Pp, T, kt), workspace, A.device)
+    c = out._c()
+    _check("pss_summarize_hybrid", _lib.pss_summarize_hybrid(
+        A.data_ptr(), A.numel(), kt, k, Pp, T, ctypes.byref(c), ws.data_ptr(), ws.numel(),
+        _stream(stream)))
+    return out
+
+
+def pss_merge_hybrid(leaves: Summaries, T: int, out: Summaries | None = None,
+                     workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """Per-process fixed trees over groups of T leaves, then the fixed tree over the roots."""
+    out = out or Summaries.empty(1, leaves.k, leaves.key_type, leaves.items.device)
+    ws = _ws(pss_hybrid_workspace_bytes(0, leaves.k, leaves.count // max(T, 1), T, leaves.key_type),
+             workspace, leaves.items.device)
+    a, b = leaves._c(), out._c()
+    _check("pss_merge_hybrid", _lib.pss_merge_hybrid(ctypes.byref(a), T, ctypes.byref(b),
+                                                     ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out

@@ -139,7 +139,7 @@ size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0 = 0,
-                             uint32_t r1 = 0xffffffffu, uint32_t qi = 0);
+                             uint32_t r1 = 0xffffffffu, uint32_t qi = 0, uint32_t T = 1);
 // partition queues in the summarize workspace: launches over disjoint ranges [r0, r1) that may be
 // in flight together use distinct qi < SS_MAX_RANGES
 constexpr uint32_t SS_MAX_RANGES = 64;

@@ -191,6 +191,7 @@ struct SumArgs {
   uint64_t n;
   uint32_t k, P;
   uint32_t r0, r1;  // this launch summarizes partitions [r0, r1) of the P-way decomposition
+  uint32_t T;       // > 1: P = Pp * T leaves of the two-level decomposition (f4)
   void* items;
   uint32_t* counts;
   uint32_t* errs;
@@ -265,8 +266,16 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     if (lane == 0) r = a.r0 + atomicAdd(a.queue, 1u);
     r = __shfl_sync(PSS_FULL, r, 0);
     if (r >= a.r1) break;
-    const uint64_t lo = (uint64_t)r * n / P;  // Alg. 1 l.3-4: r*n < 2^63 as n <= 2^31
-    const uint64_t hi = (uint64_t)(r + 1) * n / P;
+    uint64_t lo, hi;
+    if (a.T <= 1) {
+      lo = (uint64_t)r * n / P;  // Alg. 1 l.3-4: r*n < 2^63 as n <= 2^31
+      hi = (uint64_t)(r + 1) * n / P;
+    } else {  // two-level (hybrid) decomposition: process p = r / T, thread t = r % T
+      const uint64_t Pp = P / a.T, p = r / a.T, t = r % a.T;
+      const uint64_t b0 = p * n / Pp, Lp = (p + 1) * n / Pp - b0;
+      lo = b0 + t * Lp / a.T;
+      hi = b0 + (t + 1) * Lp / a.T;
+    }
     const uint32_t L = (uint32_t)(hi - lo);
 
     // ---- reset the summary
@@ -740,7 +749,7 @@ size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0,
-                             uint32_t r1, uint32_t qi) {
+                             uint32_t r1, uint32_t qi, uint32_t T) {
   SSPlan p = ss_plan(n, kb, k, P, d);
   if (r1 > P) r1 = P;
   if (r0 >= r1 || qi >= SS_MAX_RANGES) return cudaErrorInvalidValue;
@@ -753,6 +762,7 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.n = n;
   a.k = k;
   a.P = P;
+  a.T = T;
   a.r0 = r0;
   a.r1 = r1;
   a.items = items;

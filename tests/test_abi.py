@@ -175,3 +175,22 @@ def test_accuracy_validation_before_launch(pss):
     two = pss._Summ(0, 10, 2, 0x1000, 0x1000, 0x1000, 0x1000)
     assert lib.pss_accuracy(by(two), 100, dummy, dummy, dummy, dummy, None) == 1
     assert ctypes.sizeof(pss.AccuracyReport) == 56
+
+
+def test_hybrid_validation_before_launch(pss):
+    lib = pss._lib
+    by = ctypes.byref
+    dummy = ctypes.c_void_p(0x1000)
+    S = pss._Summ
+    assert pss.pss_hybrid_workspace_bytes(1 << 20, 100, 4, 3, pss.KEY_U32) > 0
+    assert pss.pss_hybrid_workspace_bytes(1 << 20, 100, 0, 3, pss.KEY_U32) == 0
+    leaves = S(0, 10, 12, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_summarize_hybrid(dummy, 100, 0, 10, 0, 3, by(leaves), dummy, 1 << 30, None) == 1
+    assert lib.pss_summarize_hybrid(dummy, 100, 0, 10, 4, 0, by(leaves), dummy, 1 << 30, None) == 1
+    assert lib.pss_summarize_hybrid(dummy, 100, 0, 10, 4, 4, by(leaves), dummy, 1 << 30, None) == 3
+    assert lib.pss_summarize_hybrid(dummy, 100, 0, 10, 4, 3, by(leaves), dummy, 16, None) == 4
+    root = S(0, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_merge_hybrid(by(leaves), 5, by(root), dummy, 1 << 30, None) == 1  # 12 % 5
+    assert lib.pss_merge_hybrid(by(leaves), 0, by(root), dummy, 1 << 30, None) == 1
+    bad = S(1, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_merge_hybrid(by(leaves), 3, by(bad), dummy, 1 << 30, None) == 3

@@ -371,3 +371,78 @@ def test_accuracy_exact_case_is_zero():
     cand = oracle.prune(root, A.size, k)
     r = oracle.accuracy(cand, root.counts[:cand.size], hist(A), A.size, k)
     assert r["are_reported"] == 0.0 and r["precision"] == 1.0 and r["recall"] == 1.0
+
+
+# ---------------------------------------------------------------- f4: hybrid tree shape
+def test_hybrid_bounds():
+    """Alg. 1's formulas among processes, then among each process's threads."""
+    assert oracle.hybrid_bounds(10, 2, 2) == [(0, 2), (2, 5), (5, 7), (7, 10)]  # by hand, P:92-95
+    assert oracle.hybrid_bounds(7, 3, 2) == [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 7)]
+    for n in (0, 1, 5, 97, 1000):
+        for Pp in (1, 2, 3, 7):
+            for T in (1, 2, 3, 5):
+                b = oracle.hybrid_bounds(n, Pp, T)
+                assert len(b) == Pp * T and b[0][0] == 0 and b[-1][1] == n
+                assert all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+        assert oracle.hybrid_bounds(n, 1, 6) == oracle.bounds(n, 6)  # S:221
+        assert oracle.hybrid_bounds(n, 6, 1) == oracle.bounds(n, 6)  # S:222
+
+
+def test_hybrid_degenerate_cases():
+    """(1, T) is Algorithm 1 with T workers, (Pp, 1) with Pp workers; with T a power
+    of two and Pp*T | n the process roots are nodes of the flat tree (R6), so the roots agree."""
+    import inputs
+    A = inputs.zipf(6000, 1.1, 3000, seed=4)
+    k = 20
+    flat = lambda P: oracle.tree(oracle.leaves(A, k, P), k).as_tuples()
+    assert oracle.hybrid(A, k, 1, 6)[1].as_tuples() == flat(6)
+    assert oracle.hybrid(A, k, 6, 1)[1].as_tuples() == flat(6)
+    assert oracle.hybrid(A, k, 3, 4)[1].as_tuples() == flat(12)
+    assert oracle.hybrid(A, k, 5, 8)[1].as_tuples() == flat(40)
+    # T = 3 is another tree shape: ((0,1),2) per process instead of R6 over 6 leaves
+    assert oracle.hybrid(A, k, 2, 3)[1].as_tuples() != flat(6)
+
+
+def test_hybrid_recall_grid():
+    """a 60-item stream over 5 items, k = 3: every item with f > 20 is reported for
+    every (Pp, T) grid (no false negatives)."""
+    rng = np.random.default_rng(60)
+    A = rng.choice(np.arange(1, 6, dtype=np.uint64), size=60, p=[0.4, 0.3, 0.1, 0.1, 0.1])
+    f = hist(A)
+    heavy = {x for x, c in f.items() if c * 3 > 60}
+    assert heavy
+    for Pp in range(1, 6):
+        for T in range(1, 6):
+            root = oracle.hybrid(A, 3, Pp, T)[1]
+            assert heavy <= set(oracle.prune(root, 60, 3).tolist()), (Pp, T)
+
+
+def _all_shapes(lo, hi):
+    if hi - lo == 1:
+        yield lo
+        return
+    for mid in range(lo + 1, hi):
+        for left in _all_shapes(lo, mid):
+            for right in _all_shapes(mid, hi):
+                yield (left, right)
+
+
+def test_reduction_order_robustness():
+    """every binary tree shape over <= 5 worker summaries keeps the guarantees: recall 1,
+    f <= f_hat <= f + err, err <= n/k (COMBINE is commutative, so ordered shapes cover all)."""
+    import inputs
+    for seed in range(6):
+        A = inputs.zipf(400, 1.2, 40, seed=seed)
+        k = 4
+        f = hist(A)
+        heavy = {x for x, c in f.items() if c * k > A.size}
+        for P in range(1, 6):
+            lv = oracle.leaves(A, k, P)
+
+            def red(t):
+                return lv[t] if isinstance(t, int) else oracle.combine(red(t[0]), red(t[1]), k)
+            for shape in _all_shapes(0, P):
+                root = red(shape)
+                assert heavy <= set(oracle.prune(root, A.size, k).tolist())
+                for x, c, e in root.as_tuples():
+                    assert f.get(x, 0) <= c <= f.get(x, 0) + e and e <= A.size // k
