@@ -203,6 +203,28 @@ def config_of(w, P, gpus):
     return d
 
 
+# ------------------------------------------------------------------------------ accuracy (f3)
+def accuracy_leg(pss, runner, d_A, n, k):
+    """The paper's accuracy metrics of the last timed step's answer, against the exact
+    k-majority set computed without Space Saving (pss_exact_kmajority, timed here with CUDA
+    events: a second exact method, two passes over A). Not part of the timed step."""
+    import torch
+    st = torch.cuda.current_stream()
+    ts = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        _, _, n_true, over = pss.pss_exact_kmajority(d_A, k)
+        b.record(st)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    cand, n_cand = runner.cand
+    rep = pss.pss_accuracy(runner.top, n, n_cand, runner.exact, n_true).as_dict()
+    rep["exact_kmajority_ms"] = round(min(ts), 3)
+    rep["exact_kmajority_overflow"] = int(over.item())
+    return rep
+
+
 # ------------------------------------------------------------------------------ stream leg (f2)
 def stream_leg(pss, w, P, h_A, d_A, passes, dev):
     """On-line ingestion (pss_stream_*): one stream of passes * n keys (the
@@ -386,6 +408,8 @@ def main():
             "gpu_launches": runner.launches_per_step * K,
             "clocks": clk.summary(),
             "result_len": ln}
+    if world == 1:
+        line["accuracy"] = accuracy_leg(pss, runner, d_A, n, k)
     if world == 1 and not args.no_stream:
         line["stream"] = stream_leg(pss, w, P, h_A, d_A, args.stream_passes, dev)
     if world == 1 and not args.no_cpu_baseline:
