@@ -6,9 +6,9 @@
 // LHH_B items; if f(x) > n/k then f_r(x) > L_r/k in at least one sub-block r (otherwise
 // f(x) = sum_r f_r(x) <= sum_r L_r/k = n/k). Pass 1 builds every sub-block's exact histogram in
 // shared memory (a CTA-wide hash table, equal keys of a warp instruction aggregated with
-// __match_any_sync) and inserts its locally heavy keys into a global hash set G; pass 2 rebuilds
-// the histograms and adds the local count of every key found in G, so G holds exact counts of
-// all its keys; the entries with count >= floor(n/k) + 1 are ranked by K5 (result_kernel).
+// __match_any_sync) and inserts its locally heavy keys into a global hash set G; G is compacted
+// into a candidate list whose exact counts K4 (verify_kernel, the off-line counting scan) takes in
+// one more pass; the candidates with count >= floor(n/k) + 1 are ranked by K5 (result_kernel).
 // No step uses Space Saving, so the set is an independent truth for recall.
 #include <algorithm>
 
@@ -38,7 +38,6 @@ template <typename KT>
 struct GSet {  // global open-addressing set: state 0 empty, 1 being written, 2 ready
   KT* keys;
   uint32_t* state;
-  unsigned long long* counts;
   uint32_t mask;
   uint32_t* overflow;
 };
@@ -73,19 +72,7 @@ __device__ void gset_insert(const GSet<KT>& g, KT x) {
   atomicExch(g.overflow, 1u);
 }
 
-// pass 2: no writer is running, every entry is 0 or 2
 template <typename KT>
-__device__ __forceinline__ int64_t gset_find(const GSet<KT>& g, KT x) {
-  uint32_t h = mix_hash(x) & g.mask;
-  for (uint32_t probe = 0; probe <= g.mask; ++probe) {
-    if (g.state[h] == 0) return -1;
-    if (g.keys[h] == x) return h;
-    h = (h + 1) & g.mask;
-  }
-  return -1;
-}
-
-template <typename KT, int PASS>
 __global__ void __launch_bounds__(LHH_THREADS) lhh_kernel(const KT* __restrict__ A, uint64_t n,
                                                           uint32_t k, GSet<KT> g) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -131,30 +118,31 @@ __global__ void __launch_bounds__(LHH_THREADS) lhh_kernel(const KT* __restrict__
     for (uint32_t e = threadIdx.x; e < LHH_TS; e += LHH_THREADS) {
       const uint32_t c = cnt[e];
       if (!c) continue;
-      const KT x = keys[e];
-      if (PASS == 1) {
-        if ((uint64_t)c * k > L) gset_insert(g, x);  // f_r(x) > L_r / k
-      } else {
-        const int64_t j = gset_find(g, x);
-        if (j >= 0) atomicAdd(&g.counts[j], (unsigned long long)c);
-      }
+      if ((uint64_t)c * k > L) gset_insert(g, keys[e]);  // f_r(x) > L_r / k
     }
     __syncthreads();
   }
 }
 
-// entries of G with count >= thr (at most k - 1 of them: their counts sum to <= n)
+// the keys of G as a dense candidate list
 template <typename KT>
-__global__ void gset_collect_kernel(GSet<KT> g, uint64_t thr, uint32_t cap, KT* cand,
-                                    uint64_t* exact, uint32_t* n_out) {
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= g.mask; e += gridDim.x * blockDim.x) {
-    if (g.state[e] != 2) continue;
-    const uint64_t c = g.counts[e];
-    if (c < thr) continue;
+__global__ void gset_compact_kernel(GSet<KT> g, KT* list, uint32_t* n_list) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= g.mask; e += gridDim.x * blockDim.x)
+    if (g.state[e] == 2) list[atomicAdd(n_list, 1u)] = g.keys[e];
+}
+
+// the candidates with exact count >= thr (fewer than k: their counts sum to <= n)
+template <typename KT>
+__global__ void kmaj_filter_kernel(const KT* list, const uint64_t* exact, const uint32_t* n_list,
+                                   uint64_t thr, uint32_t cap, KT* cand, uint64_t* cexact,
+                                   uint32_t* n_out) {
+  const uint32_t nl = *n_list;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += gridDim.x * blockDim.x) {
+    if (exact[j] < thr) continue;
     const uint32_t p = atomicAdd(n_out, 1u);
     if (p < cap) {
-      cand[p] = g.keys[e];
-      exact[p] = c;
+      cand[p] = list[j];
+      cexact[p] = exact[j];
     }
   }
 }
@@ -216,10 +204,10 @@ __global__ void __launch_bounds__(1024) accuracy_kernel(const uint32_t* fhat, ui
 }
 
 struct ExLayout {
-  size_t keys, state, counts, cand, exact, ncand, overflow, total;
+  size_t keys, state, nlist, ncand, overflow, list, lexact, cand, exact, vws, total;
   uint32_t cap;
 };
-ExLayout ex_layout(int kb, uint64_t n, uint32_t k) {
+ExLayout ex_layout(int kb, uint64_t n, uint32_t k, const DevInfo& d) {
   // G holds the locally heavy keys: at most n*k/LHH_B distinct ones (each has f > LHH_B/k);
   // capacity 2x that bound, between 2^12 and 2^24 entries (overflow is reported)
   const double bound = std::min<double>((double)n, (double)n * k / LHH_B);
@@ -229,12 +217,15 @@ ExLayout ex_layout(int kb, uint64_t n, uint32_t k) {
   L.cap = cap;
   Bump b;
   L.keys = b.take<unsigned char>((size_t)cap * kb);
-  L.state = b.take<uint32_t>(cap);
-  L.counts = b.take<unsigned long long>(cap);
-  L.cand = b.take<unsigned char>((size_t)k * kb);
-  L.exact = b.take<uint64_t>(k);
+  L.state = b.take<uint32_t>(cap);  // state .. overflow are cleared by one memset
+  L.nlist = b.take<uint32_t>(1);
   L.ncand = b.take<uint32_t>(1);
   L.overflow = b.take<uint32_t>(1);
+  L.list = b.take<unsigned char>((size_t)cap * kb);
+  L.lexact = b.take<uint64_t>(cap);
+  L.cand = b.take<unsigned char>((size_t)k * kb);
+  L.exact = b.take<uint64_t>(k);
+  L.vws = b.take<unsigned char>(verify_ws(kb, cap, d));
   L.total = b.bytes();
   return L;
 }
@@ -244,44 +235,48 @@ cudaError_t exact_run(const KT* A, uint64_t n, uint32_t k, void* out_items, uint
                       uint32_t* out_len, uint32_t* d_overflow, void* ws, cudaStream_t s,
                       const DevInfo& d) {
   unsigned char* w = static_cast<unsigned char*>(ws);
-  const ExLayout L = ex_layout(sizeof(KT), n, k);
+  const ExLayout L = ex_layout(sizeof(KT), n, k, d);
   GSet<KT> g{reinterpret_cast<KT*>(w + L.keys), reinterpret_cast<uint32_t*>(w + L.state),
-             reinterpret_cast<unsigned long long*>(w + L.counts), L.cap - 1,
-             d_overflow ? d_overflow : reinterpret_cast<uint32_t*>(w + L.overflow)};
-  // state, counts, candidate count and overflow flag start at zero
-  cudaError_t e = cudaMemsetAsync(w + L.state, 0, L.cand - L.state, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w + L.ncand, 0, L.total - L.ncand, s);
+             L.cap - 1, d_overflow ? d_overflow : reinterpret_cast<uint32_t*>(w + L.overflow)};
+  uint32_t* nlist = reinterpret_cast<uint32_t*>(w + L.nlist);
+  uint32_t* ncand = reinterpret_cast<uint32_t*>(w + L.ncand);
+  KT* list = reinterpret_cast<KT*>(w + L.list);
+  uint64_t* lexact = reinterpret_cast<uint64_t*>(w + L.lexact);
+  // set states, list and candidate counts and the overflow flag start at zero
+  cudaError_t e = cudaMemsetAsync(w + L.state, 0, L.list - L.state, s);
   if (e == cudaSuccess && d_overflow) e = cudaMemsetAsync(d_overflow, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const size_t smem = LHH_TS * (sizeof(KT) + sizeof(uint32_t));
   if (n) {
-    auto k1 = lhh_kernel<KT, 1>;
-    auto k2 = lhh_kernel<KT, 2>;
+    auto k1 = lhh_kernel<KT>;
     allow_max_smem(k1, d);
-    allow_max_smem(k2, d);
     int nb = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1, LHH_THREADS, smem) != cudaSuccess ||
         nb < 1)
       nb = 1;
     const uint64_t nsb = (n + LHH_B - 1) / LHH_B;
     const int grid = (int)std::min<uint64_t>(nsb, (uint64_t)nb * d.sms);
+    const int cgrid = std::max<int>(1, (int)std::min<uint32_t>(L.cap / 256, 4 * d.sms));
     k1<<<grid, LHH_THREADS, smem, s>>>(A, n, k, g);
-    k2<<<grid, LHH_THREADS, smem, s>>>(A, n, k, g);
-    gset_collect_kernel<KT><<<std::max<int>(1, (int)std::min<uint32_t>(L.cap / 256, 4 * d.sms)),
-                              256, 0, s>>>(g, n / k + 1, k, reinterpret_cast<KT*>(w + L.cand),
-                                           reinterpret_cast<uint64_t*>(w + L.exact),
-                                           reinterpret_cast<uint32_t*>(w + L.ncand));
+    gset_compact_kernel<KT><<<cgrid, 256, 0, s>>>(g, list, nlist);
+    e = cudaGetLastError();
+    // exact counts of the candidates: K4, the off-line counting scan (one more pass over A)
+    if (e == cudaSuccess)
+      e = verify_launch(A, n, sizeof(KT), list, L.cap, nlist, lexact, w + L.vws, s, d);
+    if (e != cudaSuccess) return e;
+    kmaj_filter_kernel<KT><<<cgrid, 256, 0, s>>>(list, lexact, nlist, n / k + 1, k,
+                                                 reinterpret_cast<KT*>(w + L.cand),
+                                                 reinterpret_cast<uint64_t*>(w + L.exact), ncand);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  return result_launch(sizeof(KT), k, w + L.cand, reinterpret_cast<uint32_t*>(w + L.ncand),
-                       reinterpret_cast<uint64_t*>(w + L.exact), n, k, out_items, out_counts,
-                       out_len, s);
+  return result_launch(sizeof(KT), k, w + L.cand, ncand, reinterpret_cast<uint64_t*>(w + L.exact),
+                       n, k, out_items, out_counts, out_len, s);
 }
 
 }  // namespace
 
-size_t exact_ws(int kb, uint64_t n, uint32_t k) { return ex_layout(kb, n, k).total; }
+size_t exact_ws(int kb, uint64_t n, uint32_t k) { return ex_layout(kb, n, k, dev_info()).total; }
 
 }  // namespace pss
 
