@@ -54,7 +54,8 @@ typedef enum {
   PSS_OP_COMBINE = 2,
   PSS_OP_VERIFY = 3,
   PSS_OP_QUERY = 4,
-  PSS_OP_EXACT = 5 /* pss_exact_kmajority; P is ignored */
+  PSS_OP_EXACT = 5, /* pss_exact_kmajority; P is ignored */
+  PSS_OP_SUMMARIZE_MERGE = 6
 } pss_op;
 
 #define PSS_MAX_K 65000u
@@ -106,6 +107,20 @@ pss_status pss_summarize(const void* d_A, uint64_t n, pss_key_type kt, uint32_t 
  */
 pss_status pss_merge(const pss_summaries* leaves, pss_summaries* root, void* d_ws,
                      size_t ws_bytes, cudaStream_t stream);
+
+/*
+ * pss_summarize_merge -- pss_summarize then pss_merge (Alg. 1 l.3-7) in one call, with
+ * the same results bit for bit. The tree kernel is launched as a programmatic dependent of the
+ * leaf kernel: its CTAs take the SMs the leaf kernel's persistent CTAs leave during its last wave
+ * and combine leaves as soon as they are written (one ready flag per leaf, release/acquire), so
+ * the merge overlaps the end of the summaries instead of following them.
+ *   leaves : as for pss_summarize (count P; written, slot order).
+ *   root   : as for pss_merge (count 1; canonical order).
+ *   workspace : pss_workspace_bytes(PSS_OP_SUMMARIZE_MERGE, n, k, P, kt).
+ */
+pss_status pss_summarize_merge(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                               uint32_t P, pss_summaries* leaves, pss_summaries* root, void* d_ws,
+                               size_t ws_bytes, cudaStream_t stream);
 
 /*
  * pss_combine -- one COMBINE(S1, S2, k) (Alg. 2; prose P:112-115) for every i:

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 
 import torch
 
-__all__ = ["Summaries", "PssError", "pss_workspace_bytes", "pss_summarize", "pss_merge",
+__all__ = ["Summaries", "PssError", "pss_workspace_bytes", "pss_summarize", "pss_summarize_merge",
+           "OP_SUMMARIZE_MERGE", "pss_merge",
            "pss_combine", "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host", "lib_path",
            "KEY_U32", "KEY_U64", "OP_SUMMARIZE", "OP_MERGE", "OP_COMBINE", "OP_VERIFY", "OP_QUERY",
            "EXPORTED_SYMBOLS"]
@@ -27,9 +28,11 @@ lib_path = os.environ.get("PSS_LIB") or os.path.join(_PKG, "libpss.so")  # PSS_L
 
 KEY_U32, KEY_U64 = 0, 1
 OP_SUMMARIZE, OP_MERGE, OP_COMBINE, OP_VERIFY, OP_QUERY = range(5)
+OP_SUMMARIZE_MERGE = 6
 STATUS = {0: "PSS_OK", 1: "PSS_ERR_INVALID_ARG", 2: "PSS_ERR_UNSUPPORTED",
           3: "PSS_ERR_CAPACITY_MISMATCH", 4: "PSS_ERR_WORKSPACE_TOO_SMALL", 5: "PSS_ERR_CUDA"}
-EXPORTED_SYMBOLS = ["pss_workspace_bytes", "pss_summarize", "pss_merge", "pss_combine",
+EXPORTED_SYMBOLS = ["pss_workspace_bytes", "pss_summarize", "pss_summarize_merge", "pss_merge",
+                    "pss_combine",
                     "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host",
                     "pss_status_string", "pss_version"]
 
@@ -57,13 +60,14 @@ _lib.pss_workspace_bytes.argtypes = [_i32, _u64, _u32, _u32, _i32]
 _lib.pss_workspace_bytes.restype = _sz
 _lib.pss_summarize.argtypes = [_vp, _u64, _i32, _u32, _u32, _SP, _vp, _sz, _vp]
 _lib.pss_merge.argtypes = [_SP, _SP, _vp, _sz, _vp]
+_lib.pss_summarize_merge.argtypes = [_vp, _u64, _i32, _u32, _u32, _SP, _SP, _vp, _sz, _vp]
 _lib.pss_combine.argtypes = [_SP, _SP, _SP, _vp, _sz, _vp]
 _lib.pss_prune.argtypes = [_SP, _u64, _vp, _vp, _vp]
 _lib.pss_verify.argtypes = [_vp, _u64, _i32, _vp, _u32, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_report.argtypes = [_vp, _u32, _vp, _vp, _i32, _u64, _u32, _vp, _vp, _vp, _vp]
 _lib.pss_query.argtypes = [_vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_query_host.argtypes = [_vp, _vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
-for _f in ("pss_summarize", "pss_merge", "pss_combine", "pss_prune", "pss_verify", "pss_report",
+for _f in ("pss_summarize", "pss_summarize_merge", "pss_merge", "pss_combine", "pss_prune", "pss_verify", "pss_report",
            "pss_query", "pss_query_host"):
     getattr(_lib, _f).restype = _i32
 _lib.pss_status_string.argtypes = [_i32]
@@ -166,6 +170,22 @@ def pss_summarize(A: torch.Tensor, k: int, P: int, out: Summaries | None = None,
     _check("pss_summarize", _lib.pss_summarize(A.data_ptr(), A.numel(), kt, k, P, ctypes.byref(c),
                                                ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
+
+
+def pss_summarize_merge(A: torch.Tensor, k: int, P: int, leaves: Summaries | None = None,
+                        root: Summaries | None = None, workspace: torch.Tensor | None = None,
+                        stream=None) -> tuple[Summaries, Summaries]:
+    """pss_summarize + pss_merge in one call, the tree overlapping the leaves (include/pss.h)."""
+    A = _dev_keys(A)
+    kt = _key_type(A)
+    leaves = leaves or Summaries.empty(P, k, kt, A.device)
+    root = root or Summaries.empty(1, k, kt, A.device)
+    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE_MERGE, A.numel(), k, P, kt), workspace, A.device)
+    a, b = leaves._c(), root._c()
+    _check("pss_summarize_merge", _lib.pss_summarize_merge(
+        A.data_ptr(), A.numel(), kt, k, P, ctypes.byref(a), ctypes.byref(b), ws.data_ptr(),
+        ws.numel(), _stream(stream)))
+    return leaves, root
 
 
 def pss_merge(leaves: Summaries, out: Summaries | None = None,

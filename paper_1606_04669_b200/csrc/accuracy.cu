@@ -42,15 +42,6 @@ struct GSet {  // global open-addressing set: state 0 empty, 1 being written, 2 
   uint32_t* overflow;
 };
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 template <typename KT>
 __device__ void gset_insert(const GSet<KT>& g, KT x) {
   uint32_t h = mix_hash(x) & g.mask;

@@ -30,6 +30,47 @@ static bool summaries_ok(const pss_summaries* s) {
 
 static pss_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA; }
 
+// workspace of the fused summarize + merge: K1's, the tree's (disjoint: the two kernels overlap)
+// and one ready flag per leaf
+struct SMLayout {
+  size_t sum, merge, flags, total;
+};
+static SMLayout sm_layout(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  SMLayout L;
+  Bump b;
+  L.sum = b.take<unsigned char>(summarize_ws(n, kb, k, P, d));
+  L.merge = b.take<unsigned char>(merge_ws(kb, k, P, d));
+  L.flags = b.take<uint32_t>(P);
+  L.total = b.bytes();
+  return L;
+}
+
+// a2 + a4: K1, then the tree kernel launched as its programmatic dependent so that the tree's
+// CTAs take the SMs K1's persistent CTAs leave in its last wave and combine leaves as soon as
+// they are written (per-leaf flags); shapes the persistent tree does not cover run in order
+static cudaError_t summarize_merge_launch(const void* A, uint64_t n, int kb, uint32_t k,
+                                          uint32_t P, void* li, uint32_t* lc, uint32_t* le,
+                                          uint32_t* ls, void* ri, uint32_t* rc, uint32_t* re,
+                                          uint32_t* rs, void* ws, cudaStream_t s,
+                                          const DevInfo& d) {
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  const SMLayout L = sm_layout(n, kb, k, P, d);
+  uint32_t* flags = reinterpret_cast<uint32_t*>(w + L.flags);
+  const bool ovl = merge_tree_overlaps(kb, k, P, d) && !std::getenv("PSS_NO_OVERLAP");
+  cudaError_t e = cudaSuccess;
+  if (ovl) {
+    e = cudaMemsetAsync(flags, 0, (size_t)P * sizeof(uint32_t), s);
+    if (e == cudaSuccess) e = merge_tree_reset(kb, k, P, w + L.merge, s, d);
+  }
+  if (e == cudaSuccess)
+    e = summarize_launch(A, n, kb, k, P, li, lc, le, ls, w + L.sum, s, d, 0, 0xffffffffu, 0, 1,
+                         ovl ? flags : nullptr, ovl);
+  if (e == cudaSuccess)
+    e = merge_tree_launch(kb, k, P, li, lc, le, ls, ri, rc, re, rs, w + L.merge, s, d,
+                          ovl ? flags : nullptr);
+  return e;
+}
+
 // workspace plan of pss_query: leaves, root, candidates, exact counts, output staging, scratch
 struct QLayout {
   size_t l_items, l_counts, l_errs, l_sizes, r_items, r_counts, r_errs, r_sizes, cand, ncand,
@@ -52,8 +93,7 @@ static QLayout q_layout(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInf
   L.o_items = b.take<unsigned char>((size_t)k * kb);
   L.o_counts = b.take<uint64_t>(k);
   L.o_len = b.take<uint32_t>(1);
-  const size_t sc = std::max({summarize_ws(n, kb, k, P, d), merge_ws(kb, k, P, d),
-                              verify_ws(kb, k, d)});
+  const size_t sc = std::max({sm_layout(n, kb, k, P, d).total, verify_ws(kb, k, d)});
   L.scratch = b.take<unsigned char>(sc);
   L.total = b.bytes();
   return L;
@@ -90,6 +130,7 @@ size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_t
     case PSS_OP_VERIFY: return verify_ws(kb, k, d);
     case PSS_OP_QUERY: return q_layout(n, kb, k, P ? P : 1, d).total;
     case PSS_OP_EXACT: return exact_ws(kb, n, k);
+    case PSS_OP_SUMMARIZE_MERGE: return sm_layout(n, kb, k, P ? P : 1, d).total;
   }
   return 0;
 }
@@ -107,6 +148,25 @@ pss_status pss_summarize(const void* d_A, uint64_t n, pss_key_type kt, uint32_t 
   if (ws_bytes < summarize_ws(n, kb, k, P, d)) return PSS_ERR_WORKSPACE_TOO_SMALL;
   return cuda_status(summarize_launch(d_A, n, kb, k, P, leaves->items, leaves->counts,
                                       leaves->errs, leaves->sizes, d_ws, stream, d));
+}
+
+pss_status pss_summarize_merge(const void* d_A, uint64_t n, pss_key_type kt, uint32_t k,
+                               uint32_t P, pss_summaries* leaves, pss_summaries* root, void* d_ws,
+                               size_t ws_bytes, cudaStream_t stream) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || P == 0 || !leaves || !root || (n && !d_A) || !d_ws)
+    return PSS_ERR_INVALID_ARG;
+  if (n > PSS_MAX_N || k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (!summaries_ok(leaves) || !summaries_ok(root)) return PSS_ERR_INVALID_ARG;
+  if (leaves->k != k || leaves->key_type != (int32_t)kt || leaves->count != P ||
+      root->k != k || root->key_type != (int32_t)kt || root->count != 1)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const DevInfo d = dev_info();
+  if (ws_bytes < sm_layout(n, kb, k, P, d).total) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(summarize_merge_launch(d_A, n, kb, k, P, leaves->items, leaves->counts,
+                                            leaves->errs, leaves->sizes, root->items,
+                                            root->counts, root->errs, root->sizes, d_ws, stream,
+                                            d));
 }
 
 pss_status pss_merge(const pss_summaries* leaves, pss_summaries* root, void* d_ws,
@@ -170,41 +230,52 @@ pss_status pss_report(const void* d_cand, uint32_t n_cand, const uint32_t* d_n_c
                                    d_out_counts, d_out_len, stream));
 }
 
-static pss_status tree_and_verify(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
-                             void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
-                             unsigned char* w, const QLayout& L, cudaStream_t s,
-                             const DevInfo& d) {
-  void* li = w + L.l_items;
-  uint32_t* lc = reinterpret_cast<uint32_t*>(w + L.l_counts);
-  uint32_t* le = reinterpret_cast<uint32_t*>(w + L.l_errs);
-  uint32_t* ls = reinterpret_cast<uint32_t*>(w + L.l_sizes);
+// a5..a7 after the root: prune, verify, report
+static pss_status prune_verify(const void* d_A, uint64_t n, int kb, uint32_t k,
+                               void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                               unsigned char* w, const QLayout& L, cudaStream_t s,
+                               const DevInfo& d) {
   void* ri = w + L.r_items;
   uint32_t* rc = reinterpret_cast<uint32_t*>(w + L.r_counts);
-  uint32_t* re = reinterpret_cast<uint32_t*>(w + L.r_errs);
   uint32_t* rs = reinterpret_cast<uint32_t*>(w + L.r_sizes);
   void* cand = w + L.cand;
   uint32_t* nc = reinterpret_cast<uint32_t*>(w + L.ncand);
   uint64_t* exact = reinterpret_cast<uint64_t*>(w + L.exact);
-  void* sc = w + L.scratch;
-  cudaError_t e = merge_tree_launch(kb, k, P, li, lc, le, ls, ri, rc, re, rs, sc, s, d);
-  if (e == cudaSuccess) e = prune_launch(kb, k, ri, rc, rs, n, cand, nc, s);
-  if (e == cudaSuccess) e = verify_launch(d_A, n, kb, cand, k, nc, exact, sc, s, d);
+  cudaError_t e = prune_launch(kb, k, ri, rc, rs, n, cand, nc, s);
+  if (e == cudaSuccess) e = verify_launch(d_A, n, kb, cand, k, nc, exact, w + L.scratch, s, d);
   if (e == cudaSuccess)
     e = result_launch(kb, k, cand, nc, exact, n, k, d_out_items, d_out_counts, d_out_len, s);
   return cuda_status(e);
 }
 
-// a2 then a4..a7
+// a4..a7 over leaves already in the workspace
+static pss_status tree_and_verify(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
+                                  void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
+                                  unsigned char* w, const QLayout& L, cudaStream_t s,
+                                  const DevInfo& d) {
+  const cudaError_t e = merge_tree_launch(
+      kb, k, P, w + L.l_items, reinterpret_cast<uint32_t*>(w + L.l_counts),
+      reinterpret_cast<uint32_t*>(w + L.l_errs), reinterpret_cast<uint32_t*>(w + L.l_sizes),
+      w + L.r_items, reinterpret_cast<uint32_t*>(w + L.r_counts),
+      reinterpret_cast<uint32_t*>(w + L.r_errs), reinterpret_cast<uint32_t*>(w + L.r_sizes),
+      w + L.scratch, s, d);
+  if (e != cudaSuccess) return PSS_ERR_CUDA;
+  return prune_verify(d_A, n, kb, k, d_out_items, d_out_counts, d_out_len, w, L, s, d);
+}
+
+// a2 + a4 (overlapped) then a5..a7
 static pss_status query_impl(const void* d_A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* d_out_items, uint64_t* d_out_counts, uint32_t* d_out_len,
                              unsigned char* w, const QLayout& L, cudaStream_t s,
                              const DevInfo& d) {
-  const cudaError_t e = summarize_launch(
+  const cudaError_t e = summarize_merge_launch(
       d_A, n, kb, k, P, w + L.l_items, reinterpret_cast<uint32_t*>(w + L.l_counts),
       reinterpret_cast<uint32_t*>(w + L.l_errs), reinterpret_cast<uint32_t*>(w + L.l_sizes),
+      w + L.r_items, reinterpret_cast<uint32_t*>(w + L.r_counts),
+      reinterpret_cast<uint32_t*>(w + L.r_errs), reinterpret_cast<uint32_t*>(w + L.r_sizes),
       w + L.scratch, s, d);
   if (e != cudaSuccess) return PSS_ERR_CUDA;
-  return tree_and_verify(d_A, n, kb, k, P, d_out_items, d_out_counts, d_out_len, w, L, s, d);
+  return prune_verify(d_A, n, kb, k, d_out_items, d_out_counts, d_out_len, w, L, s, d);
 }
 
 // chunks of the pipelined host->device copy in pss_query_host (1 = copy, then compute)

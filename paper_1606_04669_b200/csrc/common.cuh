@@ -101,6 +101,25 @@ __host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) {
   return (x + a - 1) / a * a;
 }
 
+// gpu-scope acquire load / release store of a flag (producer-consumer across CTAs and kernels)
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// programmatic dependent launch: let the next kernel on the stream start (its CTAs are placed as
+// this grid's CTAs exit); it synchronises through flags, then waits for this grid before exiting
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait_prerequisites() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // canonical order (R5): count descending, then item ascending. true if (ca,ka) precedes (cb,kb).
 template <typename KT>
 __device__ __forceinline__ bool canon_before(uint32_t ca, KT ka, uint32_t cb, KT kb) {
@@ -139,17 +158,26 @@ size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0 = 0,
-                             uint32_t r1 = 0xffffffffu, uint32_t qi = 0, uint32_t T = 1);
+                             uint32_t r1 = 0xffffffffu, uint32_t qi = 0, uint32_t T = 1,
+                             uint32_t* leaf_flags = nullptr, bool pdl = false);
 // partition queues in the summarize workspace: launches over disjoint ranges [r0, r1) that may be
 // in flight together use distinct qi < SS_MAX_RANGES
 constexpr uint32_t SS_MAX_RANGES = 64;
 
 size_t merge_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d);
-// fixed binary tree over P leaves -> root (canonical)
+// fixed binary tree over P leaves -> root (canonical). With leaf_flags, the leaves may still be
+// in production (K1 sets leaf_flags[r] once leaf r is written): the tree kernel is launched as a
+// programmatic dependent of K1 and waits per leaf; merge_tree_reset must have run before K1.
 cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
                               const uint32_t* counts, const uint32_t* errs, const uint32_t* sizes,
                               void* r_items, uint32_t* r_counts, uint32_t* r_errs,
-                              uint32_t* r_sizes, void* ws, cudaStream_t s, const DevInfo& d);
+                              uint32_t* r_sizes, void* ws, cudaStream_t s, const DevInfo& d,
+                              const uint32_t* leaf_flags = nullptr);
+// true if merge_tree_launch(..., leaf_flags) overlaps K1 for this shape (persistent tree kernel)
+bool merge_tree_overlaps(int kb, uint32_t k, uint32_t P, const DevInfo& d);
+// clears the tree's node flags and task queue (before K1 when the tree overlaps it)
+cudaError_t merge_tree_reset(int kb, uint32_t k, uint32_t P, void* ws, cudaStream_t s,
+                             const DevInfo& d);
 size_t combine_ws(int kb, uint32_t k, uint32_t count, const DevInfo& d);
 cudaError_t combine_launch(int kb, uint32_t k, uint32_t count, const void* a_items,
                            const uint32_t* a_counts, const uint32_t* a_errs,

@@ -91,14 +91,6 @@ __device__ __forceinline__ void m_tick(int ph, uint32_t lv) {
 __device__ __forceinline__ void m_tick(int, uint32_t) {}
 #endif
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int NT>
 __device__ __forceinline__ uint32_t block_reduce(uint32_t v, uint32_t* red, bool is_min) {
@@ -681,6 +673,7 @@ struct TreeArgs {
   uint32_t cin[32];  // input nodes of each level
   uint32_t* flags;   // per task: 1 once its node is written
   uint32_t* queue;
+  const uint32_t* leaf_flags;  // non-null: leaf r is ready once leaf_flags[r] != 0 (K1 overlap)
 };
 
 template <typename KT, int NT>
@@ -703,8 +696,8 @@ __global__ void __launch_bounds__(NT, 3) tree_kernel(const TreeArgs ta) {
     const bool has_r = 2 * i + 1 < ta.cin[j];
     const NodeRef& in = j == 0 ? ta.leaves : nodes_in;
     const uint32_t base = j == 0 ? 0u : ta.off[j - 1];
-    if (j > 0 && threadIdx.x == 0) {  // acquire the children
-      const uint32_t* fl = ta.flags + base + 2 * i;
+    if (threadIdx.x == 0 && (j > 0 || ta.leaf_flags)) {  // acquire the children
+      const uint32_t* fl = (j > 0 ? ta.flags + base : ta.leaf_flags) + 2 * i;
       while (ld_acquire(fl) == 0 || (has_r && ld_acquire(fl + 1) == 0)) __nanosleep(64);
     }
     __syncthreads();
@@ -719,6 +712,9 @@ __global__ void __launch_bounds__(NT, 3) tree_kernel(const TreeArgs ta) {
       st_release(ta.flags + t, 1u);
     }
   }
+  // launched as a programmatic dependent of K1: complete only after K1 has (stream order for
+  // whatever follows)
+  if (ta.leaf_flags) pdl_wait_prerequisites();
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -915,16 +911,44 @@ static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo
       nb < 1)
     nb = 1;
   const int grid = (int)std::min<uint64_t>(ta.off[ta.nlev], (uint64_t)nb * d.sms);
-  kern<<<grid, NT, p.smem, s>>>(ta);
-  return cudaGetLastError();
+  if (!ta.leaf_flags) {
+    kern<<<grid, NT, p.smem, s>>>(ta);
+    return cudaGetLastError();
+  }
+  // overlapping K1: a programmatic dependent launch (K1 triggers it at its start; the tree's CTAs
+  // are placed as K1's persistent CTAs exit and wait for their leaves through leaf_flags)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta);
+}
+
+bool merge_tree_overlaps(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  return P >= 4 && !m_plan(kb, k, d).g && tree_plan(P).nlev > 0;
+}
+
+cudaError_t merge_tree_reset(int kb, uint32_t k, uint32_t P, void* ws, cudaStream_t s,
+                             const DevInfo& d) {
+  const TreeWs L = tree_ws(kb, k, P, d);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  return cudaMemsetAsync(w + L.flags, 0, (L.queue - L.flags) + sizeof(uint32_t), s);
 }
 
 cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
                               const uint32_t* counts, const uint32_t* errs, const uint32_t* sizes,
                               void* r_items, uint32_t* r_counts, uint32_t* r_errs,
-                              uint32_t* r_sizes, void* ws, cudaStream_t s, const DevInfo& d) {
+                              uint32_t* r_sizes, void* ws, cudaStream_t s, const DevInfo& d,
+                              const uint32_t* leaf_flags) {
   unsigned char* w = static_cast<unsigned char*>(ws);
   const TreeWs L = tree_ws(kb, k, P, d);
+  if (leaf_flags && !merge_tree_overlaps(kb, k, P, d)) leaf_flags = nullptr;
   const TreePlan t = tree_plan(P);
   NodeOut nodes{w + L.items, reinterpret_cast<uint32_t*>(w + L.counts),
                 reinterpret_cast<uint32_t*>(w + L.errs), reinterpret_cast<uint32_t*>(w + L.sizes)};
@@ -947,7 +971,9 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
   const MPlan p = m_plan(kb, k, d);
   if (t.nlev > 0) {
     if (!p.g) {  // all internal levels in one persistent launch
-      cudaError_t e = cudaMemsetAsync(w + L.flags, 0, (L.queue - L.flags) + sizeof(uint32_t), s);
+      cudaError_t e = cudaSuccess;
+      if (!leaf_flags)  // else cleared before K1 (merge_tree_reset)
+        e = cudaMemsetAsync(w + L.flags, 0, (L.queue - L.flags) + sizeof(uint32_t), s);
       if (e != cudaSuccess) return e;
       TreeArgs ta{};
       fill_comb_args(ta.a, kb, k, p, nullptr);
@@ -958,6 +984,7 @@ cudaError_t merge_tree_launch(int kb, uint32_t k, uint32_t P, const void* items,
       for (uint32_t i = 0; i < t.nlev; ++i) ta.cin[i] = t.cin[i];
       ta.flags = reinterpret_cast<uint32_t*>(w + L.flags);
       ta.queue = reinterpret_cast<uint32_t*>(w + L.queue);
+      ta.leaf_flags = leaf_flags;
       e = kb == 4 ? launch_tree<uint32_t>(ta, p, d, s) : launch_tree<uint64_t>(ta, p, d, s);
       if (e != cudaSuccess) return e;
     } else {  // summaries too large for shared memory: one launch per level

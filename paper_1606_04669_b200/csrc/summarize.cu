@@ -192,6 +192,8 @@ struct SumArgs {
   uint32_t k, P;
   uint32_t r0, r1;  // this launch summarizes partitions [r0, r1) of the P-way decomposition
   uint32_t T;       // > 1: P = Pp * T leaves of the two-level decomposition (f4)
+  uint32_t* leaf_flags;  // non-null: leaf_flags[r] = 1 (release) once leaf r is written
+  int pdl;               // let the tree kernel launch now (it waits on leaf_flags)
   void* items;
   uint32_t* counts;
   uint32_t* errs;
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   for (uint32_t i = kw + lane; i < kw + 2; i += 32) bm[i] = 0;  // guard words
   __syncwarp();
   uint32_t phasebits = 0;
+  if (a.pdl) pdl_launch_dependents();
 
   while (true) {
     uint32_t r = 0;
@@ -652,6 +655,11 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       oe[t] = PACKED ? (ce & ~POSM) >> cb : err[t];
     }
     if (lane == 0) a.sizes[r] = size;
+    if (a.leaf_flags) {  // publish leaf r to the overlapping tree kernel
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release(a.leaf_flags + r, 1u);
+    }
     __syncwarp();
   }
 }
@@ -749,7 +757,8 @@ size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
                              void* items, uint32_t* counts, uint32_t* errs, uint32_t* sizes,
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0,
-                             uint32_t r1, uint32_t qi, uint32_t T) {
+                             uint32_t r1, uint32_t qi, uint32_t T, uint32_t* leaf_flags,
+                             bool pdl) {
   SSPlan p = ss_plan(n, kb, k, P, d);
   if (r1 > P) r1 = P;
   if (r0 >= r1 || qi >= SS_MAX_RANGES) return cudaErrorInvalidValue;
@@ -763,6 +772,8 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.k = k;
   a.P = P;
   a.T = T;
+  a.leaf_flags = leaf_flags;
+  a.pdl = pdl ? 1 : 0;
   a.r0 = r0;
   a.r1 = r1;
   a.items = items;

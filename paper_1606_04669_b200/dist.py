@@ -19,8 +19,8 @@ import math
 
 import torch
 
-from . import (KEY_U32, OP_MERGE, OP_SUMMARIZE, OP_VERIFY, Summaries, _key_dtype, pss_merge,
-               pss_prune, pss_query_host, pss_report, pss_summarize, pss_verify,
+from . import (KEY_U32, OP_MERGE, OP_SUMMARIZE_MERGE, OP_VERIFY, Summaries, _key_dtype,
+               pss_merge, pss_prune, pss_query_host, pss_report, pss_summarize_merge, pss_verify,
                pss_workspace_bytes)
 
 
@@ -105,7 +105,7 @@ class Runner:
         self.leaves = Summaries.empty(P, k, key_type, self.dev)
         self.root = Summaries.empty(1, k, key_type, self.dev)
         self.top = Summaries.empty(1, k, key_type, self.dev) if world > 1 else self.root
-        ws = max(pss_workspace_bytes(OP_SUMMARIZE, n, k, P, key_type),
+        ws = max(pss_workspace_bytes(OP_SUMMARIZE_MERGE, n, k, P, key_type),
                  pss_workspace_bytes(OP_MERGE, 0, k, max(P, world), key_type),
                  pss_workspace_bytes(OP_VERIFY, n, k, 1, key_type))
         self.ws = torch.empty((ws,), dtype=torch.uint8, device=self.dev)
@@ -126,10 +126,11 @@ class Runner:
         s = torch.cuda.current_stream()
         if ev is not None:
             ev[0].record(s)
-        pss_summarize(A, self.k, self.P, out=self.leaves, workspace=self.ws)
+        # leaves and this rank's subtree root; the tree kernel overlaps the leaf kernel's last wave
+        pss_summarize_merge(A, self.k, self.P, leaves=self.leaves, root=self.root,
+                            workspace=self.ws)
         if ev is not None:
             ev[1].record(s)
-        pss_merge(self.leaves, out=self.root, workspace=self.ws)
         n_global = self.n * self.world
         if self.world > 1:
             gathered = gather_summaries(self.root, self.group)

@@ -41,6 +41,8 @@ def run_path(pss, A, k, P):
     cand, n_cand = pss.pss_prune(root, A.size)
     exact = pss.pss_verify(dA, cand, n_cand)
     items, counts, length = pss.pss_query(dA, k, P)
+    # the fused call (the tree kernel overlapping the leaf kernel through per-leaf flags)
+    f_leaves, f_root = pss.pss_summarize_merge(dA, k, P)
     # the same answer without Space Saving (f3's truth: local heavy hitters + exact counts)
     x_items, x_counts, x_len, x_over = pss.pss_exact_kmajority(dA, k)
     torch.cuda.synchronize()
@@ -48,7 +50,7 @@ def run_path(pss, A, k, P):
     ln = int(length.item())
     xl = int(x_len.item())
     assert int(x_over.item()) == 0
-    return dict(leaves=leaves, root=root,
+    return dict(leaves=leaves, root=root, f_leaves=f_leaves, f_root=f_root,
                 cand=cand[:nc].cpu().numpy().astype(np.uint64).tolist(),
                 exact=exact[:nc].cpu().numpy().astype(np.uint64).tolist(),
                 result=(items[:ln].cpu().numpy().astype(np.uint64).tolist(),
@@ -63,6 +65,8 @@ def assert_full_parity(pss, A, k, P, threads=8):
     for r in range(P):
         assert got["leaves"].host(r) == ref.leaves[r].as_tuples(), f"leaf {r}"
     assert got["root"].host(0) == ref.root.as_tuples(), "root"
+    assert got["f_root"].host(0) == ref.root.as_tuples(), "root (pss_summarize_merge)"
+    assert torch.equal(got["f_leaves"].sizes, got["leaves"].sizes)
     assert got["cand"] == ref.cand.tolist()
     assert got["exact"] == ref.exact.tolist()
     assert got["result"][0] == ref.result[0].tolist()
@@ -295,6 +299,9 @@ def test_full_size(pss, name):
     for r, ref in zip(sample, ref_leaves):
         assert got["leaves"].host(r) == ref.as_tuples(), f"{name} leaf {r}"
     root = got["root"].host(0)
+    assert got["f_root"].host(0) == root  # pss_summarize_merge = pss_summarize + pss_merge
+    for r in sample:
+        assert got["f_leaves"].host(r) == got["leaves"].host(r)
     items = np.array([x for x, _, _ in root], dtype=np.uint64)
     f = oracle.verify(A, items).tolist()
     assert len(root) <= k and sum(c for _, c, _ in root) <= n
