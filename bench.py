@@ -70,13 +70,13 @@ def measured_peaks():
 
 
 def ncu_traffic(workload: str):
-    """dram bytes per launch of K1 from the committed ncu --set full capture, if any."""
+    """dram bytes of one summarize+merge (K1 + tree + root COMBINE) from committed ncu captures."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    v = d.get(workload, {}).get("summarize_dram_bytes_per_launch")
+    v = d.get(workload, {}).get("summarize_merge_dram_bytes_per_launch")
     return float(v) if v is not None else None
 
 
