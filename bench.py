@@ -414,6 +414,18 @@ def main():
             "gpu_launches": runner.launches_per_step * K,
             "clocks": clk.summary(),
             "result_len": ln}
+    # K6: the attainable HBM read bandwidth on the same array (128-bit streaming reads)
+    probe_ms = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        pss.pss_read_probe(d_A)
+        b.record(stream)
+        torch.cuda.synchronize()
+        probe_ms.append(a.elapsed_time(b))
+    read_gbs = n * kb / (min(probe_ms[1:]) * 1e-3) / 1e9
+    roof["read_probe_gbs"] = round(read_gbs, 1)
+    roof["frac_of_read_probe"] = round(achieved / read_gbs, 4)
     if world == 1:
         line["accuracy"] = accuracy_leg(pss, runner, d_A, n, k)
     if world == 1 and not args.no_stream:

@@ -311,6 +311,15 @@ pss_status pss_summarize_hybrid(const void* d_A, uint64_t n, pss_key_type kt, ui
 pss_status pss_merge_hybrid(const pss_summaries* leaves, uint32_t T, pss_summaries* root,
                             void* d_ws, size_t ws_bytes, cudaStream_t stream);
 
+/*
+ * pss_read_probe -- K6, the read-bandwidth probe: reads the n keys of d_A
+ * once with 128-bit loads and writes their bitwise fold to *d_out (one uint32, device). Its time
+ * over the hot path's own input is the attainable HBM read bandwidth the path is compared with.
+ *   d_A : 16-byte aligned (INVALID_ARG otherwise), read-only.
+ */
+pss_status pss_read_probe(const void* d_A, uint64_t n, pss_key_type kt, uint32_t* d_out,
+                          cudaStream_t stream);
+
 /* Human-readable name of a status. */
 const char* pss_status_string(pss_status s);
 

@@ -463,3 +463,19 @@ def pss_merge_hybrid(leaves: Summaries, T: int, out: Summaries | None = None,
     _check("pss_merge_hybrid", _lib.pss_merge_hybrid(ctypes.byref(a), T, ctypes.byref(b),
                                                      ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
+
+
+# ---- K6 read-bandwidth probe (include/pss.h: pss_read_probe) -------------------------------
+_lib.pss_read_probe.argtypes = [_vp, _u64, _i32, _vp, _vp]
+_lib.pss_read_probe.restype = _i32
+EXPORTED_SYMBOLS += ["pss_read_probe"]
+__all__ += ["pss_read_probe"]
+
+
+def pss_read_probe(A: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Reads A once with 128-bit loads (the attainable HBM read bandwidth); returns the fold."""
+    A = _dev_keys(A)
+    out = out if out is not None else torch.zeros((1,), dtype=torch.uint32, device=A.device)
+    _check("pss_read_probe", _lib.pss_read_probe(A.data_ptr(), A.numel(), _key_type(A),
+                                                 out.data_ptr(), _stream(stream)))
+    return out

@@ -194,3 +194,10 @@ def test_hybrid_validation_before_launch(pss):
     assert lib.pss_merge_hybrid(by(leaves), 0, by(root), dummy, 1 << 30, None) == 1
     bad = S(1, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
     assert lib.pss_merge_hybrid(by(leaves), 3, by(bad), dummy, 1 << 30, None) == 3
+
+
+def test_read_probe_validation(pss):
+    lib = pss._lib
+    assert lib.pss_read_probe(ctypes.c_void_p(0x1004), 10, 0, ctypes.c_void_p(0x1000), None) == 1
+    assert lib.pss_read_probe(ctypes.c_void_p(0x1000), 10, 0, None, None) == 1
+    assert lib.pss_read_probe(ctypes.c_void_p(0x1000), 10, 9, ctypes.c_void_p(0x1000), None) == 1

@@ -327,3 +327,14 @@ def test_crowded_index_kick_and_rehash_paths(pss, load, monkeypatch):
                           (100_000, 1000, 2, 1.1, 1e8)]:
         A = inputs.zipf(n, s, U, seed=n + k)
         assert_full_parity(pss, A, k, P)
+
+
+def test_read_probe(pss):
+    """K6 reads every byte of A: its fold is the XOR of A's 32-bit words (ragged 16-byte tails)."""
+    for n, kb in [(0, 4), (1, 4), (7, 4), (1 << 20, 4), (12345, 8), (3, 8)]:
+        A = np.random.default_rng(n).integers(0, 2**32, size=n * kb // 4, dtype=np.uint64)
+        words = A.astype(np.uint32)
+        keys = words if kb == 4 else words.view(np.uint64)
+        got = int(pss.pss_read_probe(torch.from_numpy(keys).cuda()).item())
+        want = int(np.bitwise_xor.reduce(words)) if words.size else 0
+        assert got == want, (n, kb)
