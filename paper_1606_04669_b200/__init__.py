@@ -18,8 +18,8 @@ from dataclasses import dataclass
 import torch
 
 __all__ = ["Summaries", "PssError", "pss_workspace_bytes", "pss_summarize", "pss_summarize_merge",
-           "OP_SUMMARIZE_MERGE", "pss_merge",
-           "pss_combine", "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host", "lib_path",
+           "OP_SUMMARIZE_MERGE", "pss_merge", "pss_combine", "pss_prune", "pss_verify",
+           "pss_report", "pss_query", "pss_query_host", "lib_path",
            "KEY_U32", "KEY_U64", "OP_SUMMARIZE", "OP_MERGE", "OP_COMBINE", "OP_VERIFY", "OP_QUERY",
            "EXPORTED_SYMBOLS"]
 
@@ -67,8 +67,8 @@ _lib.pss_verify.argtypes = [_vp, _u64, _i32, _vp, _u32, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_report.argtypes = [_vp, _u32, _vp, _vp, _i32, _u64, _u32, _vp, _vp, _vp, _vp]
 _lib.pss_query.argtypes = [_vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_query_host.argtypes = [_vp, _vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
-for _f in ("pss_summarize", "pss_summarize_merge", "pss_merge", "pss_combine", "pss_prune", "pss_verify", "pss_report",
-           "pss_query", "pss_query_host"):
+for _f in ("pss_summarize", "pss_summarize_merge", "pss_merge", "pss_combine", "pss_prune",
+           "pss_verify", "pss_report", "pss_query", "pss_query_host"):
     getattr(_lib, _f).restype = _i32
 _lib.pss_status_string.argtypes = [_i32]
 _lib.pss_status_string.restype = ctypes.c_char_p

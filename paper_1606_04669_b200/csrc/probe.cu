@@ -32,8 +32,9 @@ __global__ void __launch_bounds__(PROBE_THREADS) read_probe_kernel(const uint4* 
     const uint4 x = __ldcs(v + i);
     acc ^= x.x ^ x.y ^ x.z ^ x.w;
   }
-  if (blockIdx.x == 0)
-    for (uint32_t t = threadIdx.x; t < ntail; t += PROBE_THREADS) acc ^= (uint32_t)tail[t] << (8 * (t & 3));
+  if (blockIdx.x == 0)  // the last bytes of a length that is not a multiple of 16
+    for (uint32_t t = threadIdx.x; t < ntail; t += PROBE_THREADS)
+      acc ^= (uint32_t)tail[t] << (8 * (t & 3));
   acc = __reduce_xor_sync(PSS_FULL, acc);
   if ((threadIdx.x & 31) == 0) atomicXor(out, acc);
 }
