@@ -677,7 +677,7 @@ struct TreeArgs {
 };
 
 template <typename KT, int NT>
-__global__ void __launch_bounds__(NT, 3) tree_kernel(const TreeArgs ta) {
+__global__ void __launch_bounds__(NT, 1536 / NT) tree_kernel(const TreeArgs ta) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t red[3 * (NT / 32)];
   __shared__ uint32_t hist[260 + 2 * 258];
@@ -901,9 +901,12 @@ size_t merge_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
 }
 
 template <typename KT>
+#ifndef PSS_TREE_NT
+#define PSS_TREE_NT 512
+#endif
 static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo& d,
                                cudaStream_t s) {
-  constexpr int NT = 512;
+  constexpr int NT = PSS_TREE_NT;
   auto kern = tree_kernel<KT, NT>;
   allow_max_smem(kern, d);
   int nb = 0;
