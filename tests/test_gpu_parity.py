@@ -338,3 +338,18 @@ def test_read_probe(pss):
         got = int(pss.pss_read_probe(torch.from_numpy(keys).cuda()).item())
         want = int(np.bitwise_xor.reduce(words)) if words.size else 0
         assert got == want, (n, kb)
+
+
+def test_summarize_merge_repeatable(pss):
+    """The overlapped call releases leaves to the tree kernel through flags cleared before every
+    launch: back-to-back calls on one stream (no host sync) give the same leaves and root."""
+    for n, k, P in [(1 << 20, 100, 64), (300_000, 1000, 17), (2_000_000, 50, 256)]:
+        A = torch.from_numpy(inputs.zipf(n, 1.1, 1e6, seed=n + P)).cuda()
+        ref_l, ref_r = pss.pss_summarize_merge(A, k, P)
+        ref = (ref_r.host(0), ref_l.sizes.clone(), ref_l.counts.clone())
+        outs = [pss.pss_summarize_merge(A, k, P) for _ in range(8)]
+        torch.cuda.synchronize()
+        for l2, r2 in outs:
+            assert r2.host(0) == ref[0]
+            assert torch.equal(l2.sizes, ref[1]) and torch.equal(l2.counts, ref[2])
+        assert ref[0] == pss.pss_merge(pss.pss_summarize(A, k, P)).host(0)
