@@ -6,9 +6,12 @@
 // LHH_B items; if f(x) > n/k then f_r(x) > L_r/k in at least one sub-block r (otherwise
 // f(x) = sum_r f_r(x) <= sum_r L_r/k = n/k). Pass 1 builds every sub-block's exact histogram in
 // shared memory (a CTA-wide hash table, equal keys of a warp instruction aggregated with
-// __match_any_sync) and inserts its locally heavy keys into a global hash set G; G is compacted
-// into a candidate list whose exact counts K4 (verify_kernel, the off-line counting scan) takes in
-// one more pass; the candidates with count >= floor(n/k) + 1 are ranked by K5 (result_kernel).
+// __match_any_sync) and inserts its locally heavy keys into a global hash set G. Pass 2 counts
+// G's keys exactly, by the candidate count (decided on the device): up to K4_MAX_CAND, G is
+// compacted into a candidate list and K4 (verify_kernel, the off-line counting scan) counts it;
+// beyond (k >= 4096 makes every key of a sub-block locally heavy), the per-sub-block histograms are
+// rebuilt and each local count is added to its key's entry of G. The candidates with count >=
+// floor(n/k) + 1 are ranked by K5 (result_kernel).
 // No step uses Space Saving, so the set is an independent truth for recall.
 #include <algorithm>
 
@@ -22,6 +25,8 @@ constexpr uint32_t LHH_B = 4096;        // items per sub-block
 constexpr uint32_t LHH_TS = 8192;       // shared hash-table entries (load <= 0.5)
 constexpr uint32_t LHH_THREADS = 512;
 constexpr uint32_t CLAIM = 0xffffffffu; // a shared entry being claimed (counts are <= LHH_B)
+// K4 builds its candidate table serially: beyond this many candidates pass 2 is the histogram one
+constexpr uint32_t K4_MAX_CAND = 32768;
 
 __device__ __forceinline__ uint32_t mix_hash(uint32_t x) {
   x ^= x >> 16;
@@ -38,6 +43,7 @@ template <typename KT>
 struct GSet {  // global open-addressing set: state 0 empty, 1 being written, 2 ready
   KT* keys;
   uint32_t* state;
+  unsigned long long* counts;  // pass 2 by histograms: exact counts
   uint32_t mask;
   uint32_t* overflow;
 };
@@ -63,9 +69,24 @@ __device__ void gset_insert(const GSet<KT>& g, KT x) {
   atomicExch(g.overflow, 1u);
 }
 
+// pass 2 by histograms: no writer is running, every entry is 0 or 2
 template <typename KT>
+__device__ __forceinline__ int64_t gset_find(const GSet<KT>& g, KT x) {
+  uint32_t h = mix_hash(x) & g.mask;
+  for (uint32_t probe = 0; probe <= g.mask; ++probe) {
+    if (g.state[h] == 0) return -1;
+    if (g.keys[h] == x) return h;
+    h = (h + 1) & g.mask;
+  }
+  return -1;
+}
+
+// PASS 1: locally heavy keys into G. PASS 2 (runs only if *run != 0): local counts into G.counts
+template <typename KT, int PASS>
 __global__ void __launch_bounds__(LHH_THREADS) lhh_kernel(const KT* __restrict__ A, uint64_t n,
-                                                          uint32_t k, GSet<KT> g) {
+                                                          uint32_t k, GSet<KT> g,
+                                                          const uint32_t* run) {
+  if (PASS == 2 && *run == 0) return;
   extern __shared__ __align__(16) unsigned char smem[];
   KT* keys = reinterpret_cast<KT*>(smem);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + LHH_TS * sizeof(KT));
@@ -109,7 +130,12 @@ __global__ void __launch_bounds__(LHH_THREADS) lhh_kernel(const KT* __restrict__
     for (uint32_t e = threadIdx.x; e < LHH_TS; e += LHH_THREADS) {
       const uint32_t c = cnt[e];
       if (!c) continue;
-      if ((uint64_t)c * k > L) gset_insert(g, keys[e]);  // f_r(x) > L_r / k
+      if (PASS == 1) {
+        if ((uint64_t)c * k > L) gset_insert(g, keys[e]);  // f_r(x) > L_r / k
+      } else {
+        const int64_t j = gset_find(g, keys[e]);
+        if (j >= 0) atomicAdd(&g.counts[j], (unsigned long long)c);
+      }
     }
     __syncthreads();
   }
@@ -120,6 +146,28 @@ template <typename KT>
 __global__ void gset_compact_kernel(GSet<KT> g, KT* list, uint32_t* n_list) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= g.mask; e += gridDim.x * blockDim.x)
     if (g.state[e] == 2) list[atomicAdd(n_list, 1u)] = g.keys[e];
+}
+
+// which pass 2 runs: route[0] = the list length K4 counts (0: none), route[1] = 1 for histograms
+__global__ void kmaj_route_kernel(const uint32_t* n_list, uint32_t* route) {
+  const uint32_t nl = *n_list;
+  route[0] = nl <= K4_MAX_CAND ? nl : 0u;
+  route[1] = nl > K4_MAX_CAND ? 1u : 0u;
+}
+
+// histogram pass 2: the entries of G with count >= thr
+template <typename KT>
+__global__ void gset_collect_kernel(GSet<KT> g, const uint32_t* run, uint64_t thr, uint32_t cap,
+                                    KT* cand, uint64_t* cexact, uint32_t* n_out) {
+  if (*run == 0) return;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= g.mask; e += gridDim.x * blockDim.x) {
+    if (g.state[e] != 2 || g.counts[e] < thr) continue;
+    const uint32_t p = atomicAdd(n_out, 1u);
+    if (p < cap) {
+      cand[p] = g.keys[e];
+      cexact[p] = g.counts[e];
+    }
+  }
 }
 
 // the candidates with exact count >= thr (fewer than k: their counts sum to <= n)
@@ -195,7 +243,7 @@ __global__ void __launch_bounds__(1024) accuracy_kernel(const uint32_t* fhat, ui
 }
 
 struct ExLayout {
-  size_t keys, state, nlist, ncand, overflow, list, lexact, cand, exact, vws, total;
+  size_t keys, state, counts, nlist, ncand, overflow, route, list, lexact, cand, exact, vws, total;
   uint32_t cap;
 };
 ExLayout ex_layout(int kb, uint64_t n, uint32_t k, const DevInfo& d) {
@@ -208,15 +256,17 @@ ExLayout ex_layout(int kb, uint64_t n, uint32_t k, const DevInfo& d) {
   L.cap = cap;
   Bump b;
   L.keys = b.take<unsigned char>((size_t)cap * kb);
-  L.state = b.take<uint32_t>(cap);  // state .. overflow are cleared by one memset
+  L.state = b.take<uint32_t>(cap);  // state .. route are cleared by one memset
+  L.counts = b.take<unsigned long long>(cap);
   L.nlist = b.take<uint32_t>(1);
   L.ncand = b.take<uint32_t>(1);
   L.overflow = b.take<uint32_t>(1);
+  L.route = b.take<uint32_t>(2);
   L.list = b.take<unsigned char>((size_t)cap * kb);
   L.lexact = b.take<uint64_t>(cap);
   L.cand = b.take<unsigned char>((size_t)k * kb);
   L.exact = b.take<uint64_t>(k);
-  L.vws = b.take<unsigned char>(verify_ws(kb, cap, d));
+  L.vws = b.take<unsigned char>(verify_ws(kb, std::min(cap, K4_MAX_CAND), d));
   L.total = b.bytes();
   return L;
 }
@@ -228,7 +278,9 @@ cudaError_t exact_run(const KT* A, uint64_t n, uint32_t k, void* out_items, uint
   unsigned char* w = static_cast<unsigned char*>(ws);
   const ExLayout L = ex_layout(sizeof(KT), n, k, d);
   GSet<KT> g{reinterpret_cast<KT*>(w + L.keys), reinterpret_cast<uint32_t*>(w + L.state),
-             L.cap - 1, d_overflow ? d_overflow : reinterpret_cast<uint32_t*>(w + L.overflow)};
+             reinterpret_cast<unsigned long long*>(w + L.counts), L.cap - 1,
+             d_overflow ? d_overflow : reinterpret_cast<uint32_t*>(w + L.overflow)};
+  uint32_t* route = reinterpret_cast<uint32_t*>(w + L.route);
   uint32_t* nlist = reinterpret_cast<uint32_t*>(w + L.nlist);
   uint32_t* ncand = reinterpret_cast<uint32_t*>(w + L.ncand);
   KT* list = reinterpret_cast<KT*>(w + L.list);
@@ -239,8 +291,10 @@ cudaError_t exact_run(const KT* A, uint64_t n, uint32_t k, void* out_items, uint
   if (e != cudaSuccess) return e;
   const size_t smem = LHH_TS * (sizeof(KT) + sizeof(uint32_t));
   if (n) {
-    auto k1 = lhh_kernel<KT>;
+    auto k1 = lhh_kernel<KT, 1>;
+    auto k2 = lhh_kernel<KT, 2>;
     allow_max_smem(k1, d);
+    allow_max_smem(k2, d);
     int nb = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1, LHH_THREADS, smem) != cudaSuccess ||
         nb < 1)
@@ -248,16 +302,24 @@ cudaError_t exact_run(const KT* A, uint64_t n, uint32_t k, void* out_items, uint
     const uint64_t nsb = (n + LHH_B - 1) / LHH_B;
     const int grid = (int)std::min<uint64_t>(nsb, (uint64_t)nb * d.sms);
     const int cgrid = std::max<int>(1, (int)std::min<uint32_t>(L.cap / 256, 4 * d.sms));
-    k1<<<grid, LHH_THREADS, smem, s>>>(A, n, k, g);
+    k1<<<grid, LHH_THREADS, smem, s>>>(A, n, k, g, nullptr);
     gset_compact_kernel<KT><<<cgrid, 256, 0, s>>>(g, list, nlist);
+    kmaj_route_kernel<<<1, 1, 0, s>>>(nlist, route);
     e = cudaGetLastError();
-    // exact counts of the candidates: K4, the off-line counting scan (one more pass over A)
+    // pass 2, one of two (the other's kernels return at once): K4, the off-line counting scan,
+    // over the compacted list (route[0] candidates) ...
+    const uint32_t kcap = std::min(L.cap, K4_MAX_CAND);
     if (e == cudaSuccess)
-      e = verify_launch(A, n, sizeof(KT), list, L.cap, nlist, lexact, w + L.vws, s, d);
+      e = verify_launch(A, n, sizeof(KT), list, kcap, route, lexact, w + L.vws, s, d);
     if (e != cudaSuccess) return e;
-    kmaj_filter_kernel<KT><<<cgrid, 256, 0, s>>>(list, lexact, nlist, n / k + 1, k,
+    kmaj_filter_kernel<KT><<<cgrid, 256, 0, s>>>(list, lexact, route, n / k + 1, k,
                                                  reinterpret_cast<KT*>(w + L.cand),
                                                  reinterpret_cast<uint64_t*>(w + L.exact), ncand);
+    // ... or the histograms again, adding local counts to G (route[1])
+    k2<<<grid, LHH_THREADS, smem, s>>>(A, n, k, g, route + 1);
+    gset_collect_kernel<KT><<<cgrid, 256, 0, s>>>(g, route + 1, n / k + 1, k,
+                                                  reinterpret_cast<KT*>(w + L.cand),
+                                                  reinterpret_cast<uint64_t*>(w + L.exact), ncand);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
