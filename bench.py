@@ -154,9 +154,21 @@ def oracle_sample(w, seconds: float, threads: int, A_host=None):
     dt = time.perf_counter() - t0
     desc = (f"first {S} of {w.P} blocks ({m} keys, {100.0 * m / w.n:.2f}% of n), k={w.k}: "
             f"leaves + fixed tree + prune + verify + report, oracle/pss_oracle.c via ctypes, "
-            f"leaves on {threads} threads")
+            f"leaves on {threads} threads of {cpu_model()}; one core: {chunk / t1 / 1e6:.1f} "
+            f"Mitems/s (Space Saving on one block)")
     del pl
     return m / dt, desc, threads, dt
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
 
 
 def run_reference(args):
