@@ -50,3 +50,11 @@ def test_hybrid_u64(pss):
     dA = torch.from_numpy(A).cuda()
     root = pss.pss_merge_hybrid(pss.pss_summarize_hybrid(dA, 200, 3, 5), 5)
     assert root.host(0) == oracle.hybrid(A, 200, 3, 5)[1].as_tuples()
+
+
+def test_hybrid_large_k(pss):
+    """k = 5000: K1 keeps its state in global memory and every tree level is its own launch."""
+    A = inputs.zipf(400_000, 1.1, 1e6, seed=77)
+    dA = torch.from_numpy(A).cuda()
+    root = pss.pss_merge_hybrid(pss.pss_summarize_hybrid(dA, 5000, 2, 3), 3)
+    assert root.host(0) == oracle.hybrid(A, 5000, 2, 3)[1].as_tuples()

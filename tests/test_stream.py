@@ -126,3 +126,17 @@ def test_full_size_host_stream(pss):
     u, c = torch.unique(dA.view(torch.int32), return_counts=True)  # brute-force histogram
     true = u[c * w.k > A.size].cpu().numpy().view(np.uint32).astype(np.uint64).tolist()
     assert set(true) <= cset and len(true) > 0
+
+
+def test_large_k_stream(pss):
+    """k = 5000 (global-memory K1 state, level-by-level merges) with ragged feeds."""
+    A = inputs.zipf(300_000, 1.1, 1e6, seed=78)
+    feed_and_check(pss, A, 5000, 40_000, 3, [1, 39_999, 40_001, 150_000], check_every=False)
+
+
+def test_summarize_merge_large_k(pss):
+    """The fused call falls back to the ordered path when the tree cannot run persistently."""
+    A = inputs.zipf(500_000, 1.1, 1e6, seed=79)
+    dA = torch.from_numpy(A).cuda()
+    leaves, root = pss.pss_summarize_merge(dA, 5000, 6)
+    assert root.host(0) == oracle.tree(oracle.leaves(A, 5000, 6, threads=6), 5000).as_tuples()
