@@ -30,7 +30,8 @@ struct StreamLayout {
   size_t b_items, b_counts, b_errs, b_sizes;          // batch_leaves leaf summaries
   size_t staging;                                     // leaf_len keys: the partial leaf
   size_t hostbuf;                                     // 2 x batch_leaves * leaf_len keys (feed_host)
-  size_t scratch, total;
+  size_t flags;                                       // batch_leaves ready flags (K1 -> tree)
+  size_t sumscratch, scratch, total;                  // K1's and the tree's (they overlap)
 };
 constexpr uint32_t STACK_LEVELS = 64;
 
@@ -52,10 +53,11 @@ StreamLayout stream_layout(int kb, uint32_t k, uint32_t leaf_len, uint32_t batch
   L.b_sizes = b.take<uint32_t>(batch);
   L.staging = b.take<unsigned char>((size_t)leaf_len * kb);
   L.hostbuf = b.take<unsigned char>((size_t)2 * batch * leaf_len * kb);
+  L.flags = b.take<uint32_t>(batch);
   const uint64_t nb = (uint64_t)batch * leaf_len;
-  const size_t sc = std::max({summarize_ws(nb, kb, k, batch, d), summarize_ws(leaf_len, kb, k, 1, d),
-                              merge_ws(kb, k, batch, d), combine_ws(kb, k, 1, d)});
-  L.scratch = b.take<unsigned char>(sc);
+  L.sumscratch = b.take<unsigned char>(
+      std::max(summarize_ws(nb, kb, k, batch, d), summarize_ws(leaf_len, kb, k, 1, d)));
+  L.scratch = b.take<unsigned char>(std::max(merge_ws(kb, k, batch, d), combine_ws(kb, k, 1, d)));
   L.total = b.bytes();
   return L;
 }
@@ -85,29 +87,34 @@ struct StreamCtx {
   One leaf(uint32_t i) const { return region(L.b_items, L.b_counts, L.b_errs, L.b_sizes, i); }
   void* scratch() const { return w + L.scratch; }
 
-  // the R6 root of `cnt` consecutive summaries starting at `first` (cnt = 1: canonical copy)
-  cudaError_t tree(const One& first, uint32_t cnt, const One& out, cudaStream_t s) const {
+  // the R6 root of `cnt` consecutive summaries starting at `first` (cnt = 1: canonical copy);
+  // with leaf_flags, a tree kernel overlapping the K1 launch that produces the leaves
+  cudaError_t tree(const One& first, uint32_t cnt, const One& out, cudaStream_t s,
+                   const uint32_t* leaf_flags = nullptr) const {
     return merge_tree_launch(kb, k, cnt, first.items, first.counts, first.errs, first.sizes,
-                             out.items, out.counts, out.errs, out.sizes, scratch(), s, d);
+                             out.items, out.counts, out.errs, out.sizes, scratch(), s, d,
+                             leaf_flags);
   }
   cudaError_t combine(const One& a, const One& b, const One& out, cudaStream_t s) const {
     return combine_launch(kb, k, 1, a.items, a.counts, a.errs, a.sizes, b.items, b.counts, b.errs,
                           b.sizes, out.items, out.counts, out.errs, out.sizes, scratch(), s, d);
   }
-  cudaError_t summarize(const void* A, uint64_t n, uint32_t P, const One& out,
-                        cudaStream_t s) const {
-    return summarize_launch(A, n, kb, k, P, out.items, out.counts, out.errs, out.sizes, scratch(),
-                            s, d);
+  cudaError_t summarize(const void* A, uint64_t n, uint32_t P, const One& out, cudaStream_t s,
+                        uint32_t* leaf_flags = nullptr) const {
+    return summarize_launch(A, n, kb, k, P, out.items, out.counts, out.errs, out.sizes,
+                            w + L.sumscratch, s, d, 0, 0xffffffffu, 0, 1, leaf_flags,
+                            leaf_flags != nullptr);
   }
 
   // push the root of the aligned block [p, p + 2^j) of complete leaves, whose 2^j leaf summaries
   // start at `first`; c = p is the number of complete leaves before the block
-  cudaError_t push_block(uint64_t p, uint32_t j, const One& first, cudaStream_t s) const {
+  cudaError_t push_block(uint64_t p, uint32_t j, const One& first, cudaStream_t s,
+                         const uint32_t* leaf_flags = nullptr) const {
     uint32_t top = j;  // carries run while the sibling (bit `top` of p) is on the stack
     while (top < STACK_LEVELS && ((p >> top) & 1u)) ++top;
     if (top >= STACK_LEVELS) return cudaErrorInvalidValue;
-    if (top == j) return tree(first, 1u << j, stack(j), s);
-    cudaError_t e = tree(first, 1u << j, tmp(0), s);
+    if (top == j) return tree(first, 1u << j, stack(j), s, leaf_flags);
+    cudaError_t e = tree(first, 1u << j, tmp(0), s, leaf_flags);
     uint32_t cur = 0;
     for (uint32_t t = j; t < top && e == cudaSuccess; ++t) {
       const One out = (t + 1 == top) ? stack(top) : tmp(cur == 1 ? 2 : 1);
@@ -117,16 +124,31 @@ struct StreamCtx {
     return e;
   }
 
-  // summarize and push `nl` complete leaves read from A (nl <= batch), the first being leaf c
+  // largest aligned power-of-two block of leaves starting at leaf p that fits in `room`
+  static uint32_t block_log(uint64_t p, uint32_t room) {
+    uint32_t j = 0;
+    while (j < 31 && ((p >> j) & 1u) == 0 && (2u << j) <= room) ++j;
+    return j;
+  }
+
+  // summarize and push `nl` complete leaves read from A (nl <= batch), the first being leaf c.
+  // The first block's tree overlaps K1 (pss_summarize_merge's scheme) when it runs persistently.
   cudaError_t push_leaves(const void* A, uint64_t c, uint32_t nl, cudaStream_t s) const {
     if (!nl) return cudaSuccess;
-    cudaError_t e = summarize(A, (uint64_t)nl * leaf_len, nl, leaf(0), s);
+    const uint32_t j0 = block_log(c, nl);
+    uint32_t* flags = reinterpret_cast<uint32_t*>(w + L.flags);
+    const bool ovl = merge_tree_overlaps(kb, k, 1u << j0, d);
+    cudaError_t e = cudaSuccess;
+    if (ovl) {
+      e = cudaMemsetAsync(flags, 0, (size_t)nl * sizeof(uint32_t), s);
+      if (e == cudaSuccess) e = merge_tree_reset(kb, k, 1u << j0, scratch(), s, d);
+    }
+    if (e == cudaSuccess)
+      e = summarize(A, (uint64_t)nl * leaf_len, nl, leaf(0), s, ovl ? flags : nullptr);
     uint32_t i = 0;
     while (i < nl && e == cudaSuccess) {
-      const uint64_t p = c + i;
-      uint32_t j = 0;  // largest aligned power-of-two block starting at p that fits
-      while (j < 31 && ((p >> j) & 1u) == 0 && i + (2u << j) <= nl) ++j;
-      e = push_block(p, j, leaf(i), s);
+      const uint32_t j = i == 0 ? j0 : block_log(c + i, nl - i);
+      e = push_block(c + i, j, leaf(i), s, i == 0 && ovl ? flags : nullptr);
       i += 1u << j;
     }
     return e;
