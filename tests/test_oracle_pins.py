@@ -446,3 +446,28 @@ def test_reduction_order_robustness():
                 assert heavy <= set(oracle.prune(root, A.size, k).tolist())
                 for x, c, e in root.as_tuples():
                     assert f.get(x, 0) <= c <= f.get(x, 0) + e and e <= A.size // k
+
+
+def test_stream_binary_counter_equals_fixed_tree():
+    """The identity the GPU stream is built on: the R6 tree over c leaves is
+    the right fold COMBINE(S_1, COMBINE(S_2, ... COMBINE(S_t, last))) over the complete subtrees
+    of the binary decomposition of c, built as a binary counter with carries. Checked against the
+    oracle's level-by-level tree for every c <= 40 (the fold itself uses only oracle.combine)."""
+    import inputs
+    k = 3
+    A = inputs.zipf(40 * 7, 1.1, 12, seed=5)
+    leaves = [oracle.space_saving(A, k, lo, hi) for lo, hi in oracle.stream_bounds(A.size, 7)]
+    for c in range(1, 41):
+        stack = {}  # level -> root of a complete subtree (binary counter)
+        for p in range(c - 1):  # push leaves 0..c-2 with carries; leaf c-1 plays the partial leaf
+            node, j = leaves[p], 0
+            while j in stack:
+                node = oracle.combine(stack.pop(j), node, k)
+                j += 1
+            stack[j] = node
+        acc = leaves[c - 1]
+        for j in sorted(stack):  # right fold, lowest level first
+            acc = oracle.combine(stack[j], acc, k)
+        if c == 1:
+            acc = oracle.canonical(acc)
+        assert acc.as_tuples() == oracle.tree(leaves[:c], k).as_tuples(), c
