@@ -430,10 +430,29 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         uint32_t b1, b2;
         key_hash<ET>(en, x, seed, NB, b1, b2, fp);
         ET e0, e1, e2, e3;
-        load_bucket(T, b1, e0, e1);
-        load_bucket(T, b2, e2, e3);
-        bool q0 = en.fp_eq(e0, fp), q1 = en.fp_eq(e1, fp), q2 = en.fp_eq(e2, fp),
-             q3 = en.fp_eq(e3, fp);
+        bool q0, q1, q2, q3;
+        if constexpr (sizeof(ET) == 2) {  // both entries of a bucket word compared at once
+          const uint32_t v1 = reinterpret_cast<const uint32_t*>(T)[b1];
+          const uint32_t v2 = reinterpret_cast<const uint32_t*>(T)[b2];
+          e0 = (ET)v1;
+          e1 = (ET)(v1 >> 16);
+          e2 = (ET)v2;
+          e3 = (ET)(v2 >> 16);
+          const uint32_t fm = (en.fmask << en.sb) * 0x10001u;  // fingerprint fields
+          const uint32_t tg = (fp << en.sb) * 0x10001u;
+          const uint32_t d1 = (v1 ^ tg) & fm, d2 = (v2 ^ tg) & fm;
+          q0 = (d1 & 0xffffu) == 0;
+          q1 = (d1 >> 16) == 0;
+          q2 = (d2 & 0xffffu) == 0;
+          q3 = (d2 >> 16) == 0;
+        } else {
+          load_bucket(T, b1, e0, e1);
+          load_bucket(T, b2, e2, e3);
+          q0 = en.fp_eq(e0, fp);
+          q1 = en.fp_eq(e1, fp);
+          q2 = en.fp_eq(e2, fp);
+          q3 = en.fp_eq(e3, fp);
+        }
         ET sel = q3 ? e3 : EMPTY;
         sel = q2 ? e2 : sel;
         sel = q1 ? e1 : sel;
@@ -473,14 +492,24 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         fbits = PACKED ? pos_bits(fi, b1) : 0u;
       };
 
-      uint32_t q = 0;  // items consumed
+      uint32_t q = 0;       // items consumed
+      uint32_t rq = roff;   // ring position of item q: (roff + q) % RING, kept incrementally
+      auto ring_at = [&](uint32_t lane_off) -> KT {
+        const uint32_t i = rq + lane_off;
+        return ring[i < RING ? i : i - RING];
+      };
+      auto advance = [&](uint32_t c) {
+        q = q + c;
+        rq += c;
+        if (rq >= RING) rq -= RING;
+      };
       // ---- fill phase: free counters are taken in slot order (R2)
       while (q < L && size < k) {
         const uint32_t nv = min(32u, L - q);
         ensure(q + nv);
         const bool act = lane < nv;
         const uint32_t amask = nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = ring[(roff + q + lane) % RING];
+        const KT x = ring_at(lane);
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
         int32_t s;
         uint32_t ce, fi, fp, fbits;
@@ -505,7 +534,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t grow = __popc(missL & pm);
         insert_all(ins, x, v, fi, fp, size + grow);
         size += grow;
-        q += c;
+        advance(c);
         SS_STAT(8, 1);
         SS_STAT(1, c);
         __syncwarp();
@@ -527,7 +556,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 #endif
         const bool act = F || lane < nv;
         const uint32_t amask = F || nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = ring[(roff + q + lane) % RING];
+        const KT x = ring_at(lane);
         // the match is issued first and its result first used after the lookups, so that its
         // latency (it grows with the number of distinct keys) overlaps them
         const uint32_t grp_all = __match_any_sync(PSS_FULL, x);
@@ -622,7 +651,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t last = __shfl_sync(PSS_FULL, myvic, (Mp ? Mp : 1) - 1);
         if (Mp) cur = last + 1;
         bmcount -= __popc(__ballot_sync(PSS_FULL, hitm)) + Mp;
-        q += c;
+        advance(c);
         SS_STAT(0, 1);
         SS_STAT(9, Mp);
         SS_STAT(1, c);
