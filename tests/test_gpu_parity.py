@@ -353,3 +353,23 @@ def test_summarize_merge_repeatable(pss):
             assert r2.host(0) == ref[0]
             assert torch.equal(l2.sizes, ref[1]) and torch.equal(l2.counts, ref[2])
         assert ref[0] == pss.pss_merge(pss.pss_summarize(A, k, P)).host(0)
+
+
+@pytest.mark.parametrize("n,k,P,s,U,kb", [
+    (3 * 65536, 600, 3, 1.1, 1e5, 4), (2 * 65536 + 17, 1023, 2, 0.9, 5e4, 4),
+    (65536, 1024, 1, 1.3, 3e4, 4), (4 * 65536, 2047, 4, 1.1, 1e6, 4),
+    (2 * 65536, 1500, 2, 1.1, 2e4, 8), (131_071 * 2, 700, 2, 1.0, 1e4, 8)])
+def test_specialized_layout_shapes(pss, n, k, P, s, U, kb):
+    """Blocks of 2^16 .. 2^17 - 1 keys with k in [512, 2047] run K1 compiled with its layout
+    constants (slot bits 10/11, count bits 17): every output against the oracle, both key types,
+    at the edges of both ranges."""
+    A = inputs.zipf(n, s, U, seed=n + k, key_bytes=kb)
+    assert_full_parity(pss, A, k, P)
+
+
+@pytest.mark.parametrize("load", [0.8])
+def test_specialized_layout_crowded_index(pss, load, monkeypatch):
+    """The kick and rehash paths of the specialized K1 (crowded index, PSS_DEBUG_INDEX_LOAD)."""
+    monkeypatch.setenv("PSS_DEBUG_INDEX_LOAD", str(load))
+    A = inputs.zipf(2 * 65536, 0.9, 2e4, seed=31)
+    assert_full_parity(pss, A, 900, 2)
