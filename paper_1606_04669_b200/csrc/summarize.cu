@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         key_hash<ET>(en, x, seed, NB, b1, b2, fp);
         ET e0, e1, e2, e3;
         bool q0, q1, q2, q3;
-        if constexpr (sizeof(ET) == 2) {  // both entries of a bucket word compared at once
+        if constexpr (sizeof(ET) == 2 && SB > 0) {  // a bucket word's two entries at once
           const uint32_t v1 = reinterpret_cast<const uint32_t*>(T)[b1];
           const uint32_t v2 = reinterpret_cast<const uint32_t*>(T)[b2];
           e0 = (ET)v1;
@@ -495,15 +495,25 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       };
 
       uint32_t q = 0;       // items consumed
-      uint32_t rq = roff;   // ring position of item q: (roff + q) % RING, kept incrementally
+      // The specialized kernel (SB > 0) keeps the ring position of item q, (roff + q) % RING,
+      // incrementally and compares both fingerprints of a bucket word at once; the same two
+      // changes measured 2-5 % slower in the runtime-layout kernel (k = 2000), which keeps the
+      // modulo and the per-entry compares.
+      uint32_t rq = roff;
       auto ring_at = [&](uint32_t lane_off) -> KT {
-        const uint32_t i = rq + lane_off;
-        return ring[i < RING ? i : i - RING];
+        if constexpr (SB > 0) {
+          const uint32_t i = rq + lane_off;
+          return ring[i < RING ? i : i - RING];
+        } else {
+          return ring[(roff + q + lane_off) % RING];
+        }
       };
       auto advance = [&](uint32_t c) {
         q = q + c;
-        rq += c;
-        if (rq >= RING) rq -= RING;
+        if constexpr (SB > 0) {
+          rq += c;
+          if (rq >= RING) rq -= RING;
+        }
       };
       // ---- fill phase: free counters are taken in slot order (R2)
       while (q < L && size < k) {
@@ -828,27 +838,21 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   if (e != cudaSuccess) return e;
   if (!p.gstate) {
     if (p.packed) {
-      // common shapes compiled with their layout constants: k in [512, 2047] (slot bits 10, 11)
-      // and blocks of 2^16 .. 2^17 - 1 keys (count bits 17)
-      const int spec = p.cb == 17 && (p.sb == 10 || p.sb == 11) ? (int)p.sb : 0;
+      // the common shape compiled with its layout constants: k in [512, 1023] (slot bits 10) and
+      // blocks of 2^16 .. 2^17 - 1 keys (count bits 17). (Slot bits 11, k in [1024, 2047], was
+      // measured too: 3 % faster on evicting inputs, 4-7 % slower on the fill-heavy C3 s >= 1.5.)
+      const int spec = p.cb == 17 && p.sb == 10 ? 10 : 0;
       if (spec == 10)
         allow_max_smem(kb == 4 ? ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17>
                                : ss_summarize_kernel<uint64_t, uint16_t, false, true, 10, 17>, d);
-      else if (spec == 11)
-        allow_max_smem(kb == 4 ? ss_summarize_kernel<uint32_t, uint16_t, false, true, 11, 17>
-                               : ss_summarize_kernel<uint64_t, uint16_t, false, true, 11, 17>, d);
       if (kb == 4) {
         if (spec == 10)
           ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17><<<grid, 32, p.smem, s>>>(a);
-        else if (spec == 11)
-          ss_summarize_kernel<uint32_t, uint16_t, false, true, 11, 17><<<grid, 32, p.smem, s>>>(a);
         else
           ss_summarize_kernel<uint32_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
       } else {
         if (spec == 10)
           ss_summarize_kernel<uint64_t, uint16_t, false, true, 10, 17><<<grid, 32, p.smem, s>>>(a);
-        else if (spec == 11)
-          ss_summarize_kernel<uint64_t, uint16_t, false, true, 11, 17><<<grid, 32, p.smem, s>>>(a);
         else
           ss_summarize_kernel<uint64_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
       }

@@ -360,9 +360,9 @@ def test_summarize_merge_repeatable(pss):
     (65536, 1024, 1, 1.3, 3e4, 4), (4 * 65536, 2047, 4, 1.1, 1e6, 4),
     (2 * 65536, 1500, 2, 1.1, 2e4, 8), (131_071 * 2, 700, 2, 1.0, 1e4, 8)])
 def test_specialized_layout_shapes(pss, n, k, P, s, U, kb):
-    """Blocks of 2^16 .. 2^17 - 1 keys with k in [512, 2047] run K1 compiled with its layout
-    constants (slot bits 10/11, count bits 17): every output against the oracle, both key types,
-    at the edges of both ranges."""
+    """Blocks of 2^16 .. 2^17 - 1 keys with k in [512, 1023] run K1 compiled with its layout
+    constants (slot bits 10, count bits 17): every output against the oracle, both key types, at
+    the edges of the range and just outside it (k = 1024, 1500, 2047: the runtime-layout kernel)."""
     A = inputs.zipf(n, s, U, seed=n + k, key_bytes=kb)
     assert_full_parity(pss, A, k, P)
 
