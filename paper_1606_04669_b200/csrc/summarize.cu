@@ -4,7 +4,7 @@
 // One warp owns one partition at a time (persistent 1-warp CTAs pull partition ids from a queue).
 // The warp streams its block of A through a shared-memory ring filled by the TMA engine
 // (cp.async.bulk + mbarrier) and applies Space Saving to 32 consecutive items per step with an
-// exact batched rule (K1):
+// exact batched rule:
 //   1. each lane looks its item up in a two-choice, two-way bucketed cuckoo index
 //      (entry = fingerprint | slot in 16 bits for k <= 4094; a lookup reads both candidate
 //      buckets with two independent loads, selects the first fingerprint match without branches
@@ -13,22 +13,18 @@
 //      popcount of the group restricted to the processed prefix;
 //   3. leaders that miss are ranked in stream order; during the fill phase they take slots
 //      size, size+1, ... (R2); once all k counters are occupied they take the lowest-index slots of
-//      B_m = {slots with count == m, the current minimum} in ascending order (R1). B_m is kept as
-//      a list of slot indices in ascending order (refilled 256 at a time from a scan of the
-//      counters); a slot stays in B_m exactly while its count is m, so stale list entries (slots
-//      hit since the list was built) are recognised by a load of the count and skipped. At the
-//      start of every step, in parallel with the lookups, lane j loads the j-th next list entry
-//      and its counter word (which also holds the position of the slot's index entry);
+//      B_m = {slots with count == m, the current minimum} in ascending order (R1). B_m is a bitmap
+//      consumed left to right through a cursor; at the start of every step, in parallel with the
+//      lookups, lane j fetches the j-th next victim slot and the index entry of its item;
 //   4. the step processes the longest prefix [0, c) of the 32 items for which this equals the
-//      sequential algorithm: c stops before the first miss that finds no victim among the fetched
-//      entries or past the last free counter, and at the later of the two positions when a
+//      sequential algorithm: c stops before the first miss that finds no victim left (B_m empty
+//      or beyond the fetched words) or the counters full, and before the first hazard where a
 //      victim slot is also hit in the window;
 //   5. hits add their multiplicity; misses evict (count m + mult, err m), free the victim's index
 //      entry and write their own entry into a free way of their buckets; a read-back settles lanes
 //      that picked the same entry, and the rare leftovers take a serial cuckoo-kick path.
 // Every step consumes >= 1 item, so the result is bit-identical to sequential Space Saving.
-// When the block length allows (blocks < 2^17 keys), a counter word holds the count in its low cb
-// bits and the position of the slot's index entry above them; errors live in their own array.
+// When the block length allows, count and error share one 32-bit word (count in the low cb bits).
 #include <cstdlib>
 #include <type_traits>
 
@@ -53,9 +49,21 @@ extern "C" int pss_debug_stats(unsigned long long* out, int reset) {
   return (int)cudaGetLastError();
 }
 namespace pss {
+// step-phase timing (debug build): wait for a value, then read the SM clock
+#define SS_TICK(acc, t, val)                                         \
+  do {                                                               \
+    uint32_t _d;                                                     \
+    asm volatile("mov.b32 %0, %1;" : "=r"(_d) : "r"((uint32_t)(val))); \
+    const long long _t = clock64() + (_d & 0);                       \
+    acc += _t - t;                                                   \
+    t = _t;                                                          \
+  } while (0)
 #else
 #define SS_STAT(i, v) \
   do {                \
+  } while (0)
+#define SS_TICK(acc, t, val) \
+  do {                       \
   } while (0)
 #endif
 
@@ -72,11 +80,8 @@ constexpr uint32_t SS_BAR_BYTES = 32;  // the ring's mbarriers (3 x 8 bytes)
 constexpr uint32_t SS_RING_BYTES = SS_NSTAGE * SS_STAGE_BYTES;
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
 constexpr uint32_t SS_K_SMALL = 4094;             // 16-bit index entries up to this k
-constexpr double SS_LOAD = 0.30;  // index load factor (live keys / entries), before the slack fill
+constexpr double SS_LOAD = 0.24;  // index load factor (live keys / entries), before the slack fill
 constexpr int SS_MAX_KICKS = 200;
-// capacity of the B_m list (slot indices) for windows of R rows of 32 items
-__host__ __device__ constexpr uint32_t ss_vq(uint32_t R) { return R <= 2 ? 256u : 512u; }
-constexpr uint32_t SS_PB = 15;    // index-position bits of a packed counter word (entries < 2^15)
 
 // Index entry layout (runtime): slot in the low sb bits, fingerprint above. A slot field of all
 // ones is never a slot (sb is chosen so that k - 1 < 2^sb - 1) and a fingerprint is never all ones,
@@ -134,25 +139,19 @@ __device__ __forceinline__ void key_hash(const Ent<ET>& en, KT x, uint32_t seed,
 // (balanced two-choice allocation); 0xffffffff if all four are occupied
 template <typename ET>
 __device__ __forceinline__ uint32_t free_entry(ET e0, ET e1, ET e2, ET e3, uint32_t b1,
-                                               uint32_t b2, uint32_t pref) {
+                                               uint32_t b2) {
   constexpr ET EMPTY = Ent<ET>::EMPTY;
-  // within a bucket the key's preferred way first (pref = a bit of its hash), so that two keys
-  // choosing one bucket in the same step take different ways half of the time
-  const uint32_t w0 = pref & 1u, w1 = w0 ^ 1u;
-  const bool f0 = (w0 ? e1 : e0) == EMPTY, f1 = (w0 ? e0 : e1) == EMPTY;
-  const bool f2 = (w0 ? e3 : e2) == EMPTY, f3 = (w0 ? e2 : e3) == EMPTY;
-  uint32_t fa = f1 ? 2 * b1 + w1 : 0xffffffffu;
-  fa = f0 ? 2 * b1 + w0 : fa;
-  uint32_t fb = f3 ? 2 * b2 + w1 : 0xffffffffu;
-  fb = f2 ? 2 * b2 + w0 : fb;
-  const bool pickb = (uint32_t)f2 + (uint32_t)f3 > (uint32_t)f0 + (uint32_t)f1;
+  uint32_t fa = e1 == EMPTY ? 2 * b1 + 1 : 0xffffffffu;
+  fa = e0 == EMPTY ? 2 * b1 : fa;
+  uint32_t fb = e3 == EMPTY ? 2 * b2 + 1 : 0xffffffffu;
+  fb = e2 == EMPTY ? 2 * b2 : fb;
+  const bool pickb = (uint32_t)(e2 == EMPTY) + (uint32_t)(e3 == EMPTY) >
+                     (uint32_t)(e0 == EMPTY) + (uint32_t)(e1 == EMPTY);
   return pickb ? fb : fa;
 }
 
-// one summary's state (shared memory, or global memory for large k); every slot-indexed array
-// holds exactly k entries (slots are < k)
 struct SSLayout {
-  size_t keys, cw, err, pos, vq, vic, T, total;
+  size_t keys, cnt, err, pos, bm, vic, T, total;
   uint32_t NB;
 };
 
@@ -165,33 +164,23 @@ static double ss_debug_load() {
   }
   return 0.0;
 }
-// experiment hook: target index load before the slack fill (sets the occupancy)
-static double ss_target_load() {
-  if (const char* s = std::getenv("PSS_SS_LOAD")) {
-    double v = std::atof(s);
-    if (v > 0.1 && v < 0.8) return v;
-  }
-  return SS_LOAD;
-}
 static uint32_t ss_buckets(uint32_t k, double load) {
   return (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * load)));
 }
 
-// kb: key bytes; eb: index entry bytes (2 or 8); errb: error bytes; packed: the entry position
-// lives in the counter word (else a pos array of 2- or 4-byte entries)
-static SSLayout ss_layout(uint32_t k, int kb, int eb, int errb, bool packed, uint32_t NB,
-                          uint32_t R) {
+static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed, uint32_t NB) {
   SSLayout L;
-  const int pb = eb == 2 ? 2 : 4;  // pos / list entry bytes
+  const size_t KP = align_up(k, 32);
   L.NB = NB;
   Bump b;
-  b.al = 16;
+  b.al = 16;  // every slot-indexed array holds exactly k entries (slots are < k)
   L.keys = b.take<unsigned char>((size_t)k * kb);
-  L.cw = b.take<uint32_t>(k);
-  L.err = b.take<unsigned char>((size_t)k * errb);
-  L.pos = packed ? L.cw : b.take<unsigned char>((size_t)k * pb);
-  L.vq = b.take<unsigned char>((size_t)ss_vq(R) * pb);
-  L.vic = b.take<uint2>(32 * R);
+  L.cnt = b.take<uint32_t>(k);
+  L.err = packed ? L.cnt : b.take<uint32_t>(k);
+  // packed counters carry their index position in the top two bits (bucket choice, way)
+  L.pos = packed ? L.cnt : b.take<unsigned char>((size_t)k * (eb == 2 ? 2 : 4));
+  L.bm = b.take<uint32_t>(KP / 32 + 2);
+  L.vic = b.take<uint32_t>(32);
   L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
   L.total = b.bytes();  // a multiple of 16
   return L;
@@ -212,18 +201,18 @@ struct SumArgs {
   uint32_t* queue;
   unsigned char* gstate;  // per-CTA state when it does not fit shared memory
   size_t gstride;
-  size_t o_cw, o_err, o_pos, o_vq, o_vic, o_T;
+  size_t o_cnt, o_err, o_pos, o_bm, o_vic, o_T;
   uint32_t NB;
-  uint32_t cb;            // PACKED: count in the low cb bits, index position above
+  uint32_t cb;            // PACKED: count in the low cb bits, error above
   uint32_t sb, fmask;     // index entry layout
 };
 
 // SB, CB > 0: the index entry's slot bits and the counter word's count bits as compile-time
-// constants (shifts and masks become immediates); 0: runtime. ERRT: the error array's type
-// (errors are <= the block length / k).
-template <typename KT, typename ET, bool GSTATE, bool PACKED, typename ERRT, int SB = 0, int CB = 0,
-          uint32_t R = 1>
-// 1-warp CTAs: __launch_bounds__(32) measured 12-15 % faster than any multi-warp bound (round 1)
+// constants (shifts and masks become immediates and free registers: 4.5 % at H); 0: runtime
+template <typename KT, typename ET, bool GSTATE, bool PACKED, int SB = 0, int CB = 0>
+// 1-warp CTAs: __launch_bounds__(32) measured 12-15 % faster than any multi-warp bound (CTAs of
+// several independent warps, sharing the per-CTA reserved shared memory, lost more than the
+// extra residency gained)
 __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   using PT = typename std::conditional<sizeof(ET) == 2, uint16_t, uint32_t>::type;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -233,32 +222,37 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   constexpr uint32_t RING = SS_NSTAGE * ST;  // ring capacity in items
   constexpr uint32_t E = 16 / sizeof(KT);  // items per 16 bytes
   constexpr ET EMPTY = Ent<ET>::EMPTY;
-  constexpr uint32_t VQ = ss_vq(R);
   const Ent<ET> en{SB ? (uint32_t)SB : a.sb, SB ? (1u << (16 - SB)) - 1u : a.fmask};
 
   KT* ring = reinterpret_cast<KT*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SS_RING_BYTES);
   unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + SS_BAR_BYTES;
   KT* keys = reinterpret_cast<KT*>(st);
-  // count; if PACKED also the position of the slot's index entry above the low cb bits
-  uint32_t* cw = reinterpret_cast<uint32_t*>(st + a.o_cw);
-  ERRT* err = reinterpret_cast<ERRT*>(st + a.o_err);
-  PT* pos = reinterpret_cast<PT*>(st + a.o_pos);  // index entry of each slot (unpacked)
-  PT* vq = reinterpret_cast<PT*>(st + a.o_vq);    // B_m list: slot indices, ascending
-  uint2* vic = reinterpret_cast<uint2*>(st + a.o_vic);  // this step's victims: (slot, entry)
+  // count; if PACKED also err << cb and the index position of the slot's entry in bits 30-31
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);
+  PT* pos = reinterpret_cast<PT*>(st + a.o_pos);               // index entry of each slot
+  uint32_t* err = reinterpret_cast<uint32_t*>(st + a.o_err);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(st + a.o_bm);
+  uint32_t* vic = reinterpret_cast<uint32_t*>(st + a.o_vic);
   ET* T = reinterpret_cast<ET*>(st + a.o_T);
 
   const KT* __restrict__ A = reinterpret_cast<const KT*>(a.A);
   const uint64_t n = a.n;
   const uint32_t k = a.k, P = a.P, NB = a.NB;
   const uint32_t NE = 2 * NB;
+  const uint32_t kw = (k + 31u) / 32u;
   const uint32_t cb = CB ? (uint32_t)CB : a.cb;
   const uint32_t CM = PACKED ? ((1u << cb) - 1u) : 0xffffffffu;
-  auto set_pos = [&](uint32_t v, uint32_t idx) {
+  constexpr uint32_t POSM = 3u << 30;
+  // index position bits of entry fi of a key whose first bucket is b1: (fi in b2) << 31 | way << 30
+  auto pos_bits = [](uint32_t fi, uint32_t b1) -> uint32_t {
+    return fi == 0xffffffffu ? 0u : (((fi >> 1) != b1 ? 2u : 0u) | (fi & 1u)) << 30;
+  };
+  auto set_pos = [&](uint32_t cv, uint32_t idx, uint32_t b1) {
     if (PACKED)
-      cw[v] = (cw[v] & CM) | (idx << cb);
+      cnt[cv] = (cnt[cv] & ~POSM) | pos_bits(idx, b1);
     else
-      pos[v] = (PT)idx;
+      pos[cv] = (PT)idx;
   };
   const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
   const uint64_t nfloor = aligned ? (n & ~(uint64_t)(E - 1)) : 0;
@@ -267,6 +261,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     for (uint32_t j = 0; j < SS_NSTAGE; ++j) mbar_init(&bars[j], 1);
     fence_mbar_init();
   }
+  for (uint32_t i = kw + lane; i < kw + 2; i += 32) bm[i] = 0;  // guard words
   __syncwarp();
   uint32_t phasebits = 0;
   if (a.pdl) pdl_launch_dependents();
@@ -290,59 +285,22 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 
     // ---- reset the summary
     for (uint32_t i = lane; i < NE; i += 32) T[i] = EMPTY;
-    uint32_t size = 0, m = 0, seed = 0;
-    uint32_t cur = 0, vlen = 0, vscan = 0;  // B_m list: next entry, length, next slot to scan
+    uint32_t size = 0, m = 0, bmcount = 0, cur = 0, seed = 0;
     __syncwarp();
 
-    // append to the list the slots t in [vscan, size) with count m, 32 at a time, until it holds
-    // more than VQ - 32 entries (the next word always fits) or every slot was scanned
-    auto scan_level = [&]() {
-      const uint32_t kw = (size + 31u) >> 5;
-      uint32_t w = vscan >> 5;
-      while (w < kw && vlen <= VQ - 32) {
+    auto new_level = [&]() {  // m = min count, B_m = {slots with count m}, cursor at slot 0
+      uint32_t mn = 0xffffffffu;
+      for (uint32_t t = lane; t < k; t += 32) mn = min(mn, cnt[t] & CM);
+      m = __reduce_min_sync(PSS_FULL, mn);
+      uint32_t tot = 0;
+      for (uint32_t w = 0; w < kw; ++w) {
         const uint32_t t = w * 32 + lane;
-        const bool at = t < size && (cw[t] & CM) == m;
-        const uint32_t b = __ballot_sync(PSS_FULL, at);
-        if (at) vq[vlen + __popc(b & ltm)] = (PT)t;
-        vlen += __popc(b);
-        ++w;
+        const uint32_t bits = __ballot_sync(PSS_FULL, t < k && (cnt[t] & CM) == m);
+        if (lane == 0) bm[w] = bits;
+        tot += __popc(bits);
       }
-      vscan = w * 32;
-    };
-    // B_m is exhausted: the next minimum is m + 1 if any counter has it (every count is > m
-    // now), otherwise a full minimum scan
-    auto new_level = [&](bool first) {
+      bmcount = tot;
       cur = 0;
-      vlen = 0;
-      vscan = 0;
-      if (!first) {
-        ++m;
-        scan_level();
-        SS_STAT(7, 1);
-      }
-      if (first || vlen == 0) {
-        uint32_t mn = 0xffffffffu;
-        for (uint32_t t = lane; t < size; t += 32) mn = min(mn, cw[t] & CM);
-        m = __reduce_min_sync(PSS_FULL, mn);
-        vscan = 0;
-        scan_level();
-      }
-      __syncwarp();
-    };
-    // fewer than a window of entries left and more slots to scan: move the rest to the front,
-    // append
-    auto refill = [&]() {
-      const uint32_t rem = vlen - cur;  // < 32 R
-      PT t[R];
-#pragma unroll
-      for (uint32_t j = 0; j < R; ++j) t[j] = 32 * j + lane < rem ? vq[cur + 32 * j + lane] : (PT)0;
-      __syncwarp();
-#pragma unroll
-      for (uint32_t j = 0; j < R; ++j)
-        if (32 * j + lane < rem) vq[32 * j + lane] = t[j];
-      vlen = rem;
-      cur = 0;
-      scan_level();
       __syncwarp();
     };
 
@@ -355,17 +313,17 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         ET f0, f1, f2, f3;
         load_bucket(T, b1, f0, f1);
         load_bucket(T, b2, f2, f3);
-        const uint32_t fi = free_entry(f0, f1, f2, f3, b1, b2, fp >> 1);
+        const uint32_t fi = free_entry(f0, f1, f2, f3, b1, b2);
         if (fi != 0xffffffffu) {
           T[fi] = en.make(fp, cv);
-          set_pos(cv, fi);
+          set_pos(cv, fi, b1);
           return true;
         }
         const uint32_t kb = (b1 != prev) ? b1 : b2;
         const uint32_t idx = 2 * kb + ((step ^ (cv & 1)) & 1);
         const ET e = T[idx];
         T[idx] = en.make(fp, cv);
-        set_pos(cv, idx);
+        set_pos(cv, idx, b1);
         cv = en.slot(e);
         cx = keys[cv];
         prev = kb;
@@ -391,12 +349,12 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
       const ET mine = en.make(fp, v);
       const bool tryfi = ins && fi != 0xffffffffu;
       // lanes that picked the same free entry: write, then read back (a match instruction here
-      // measured 12 % slower in round 1)
+      // measured 12 % slower: __match_any_sync is the costliest instruction of a step)
       ET* const tp = T + (tryfi ? fi : 0u);
       if (tryfi) *tp = mine;
       __syncwarp();
       const bool won = tryfi && *tp == mine;
-      if (!PACKED) {  // packed counters were written with the position fi
+      if (!PACKED) {  // packed counters were written with the position bits of fi
         PT* const pp = pos + v;
         if (won) *pp = (PT)fi;
       }
@@ -477,9 +435,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         }
       };
 
-      // lookup of x: slot s (-1 if not monitored), its counter word ce, the free entry fi of its
-      // buckets (insert target) and its fingerprint fp
-      auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp) {
+      // lookup of x: slot s (-1 if not monitored), its packed count ce, the first free entry fi
+      // of its buckets (insert target) and its fingerprint fp
+      auto lookup = [&](KT x, bool act, int32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp,
+                        uint32_t& fbits) {
         uint32_t b1, b2;
         key_hash<ET>(en, x, seed, NB, b1, b2, fp);
         ET e0, e1, e2, e3;
@@ -512,7 +471,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         sel = q0 ? e0 : sel;
         const uint32_t t0 = sel == EMPTY ? 0u : en.slot(sel);
         const KT kx = keys[t0];
-        ce = cw[t0];
+        ce = cnt[t0];
         const bool hit = act && sel != EMPTY && kx == x;
         s = hit ? (int32_t)t0 : -1;
         // a fingerprint match whose key differs: check the other matches in order
@@ -535,68 +494,21 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
               const uint32_t t = en.slot(nx);
               if (keys[t] == x) {
                 s = (int32_t)t;
-                ce = cw[t];
+                ce = cnt[t];
                 amb = false;
               }
             }
           }
         }
-        fi = free_entry(e0, e1, e2, e3, b1, b2, fp >> 1);
+        fi = free_entry(e0, e1, e2, e3, b1, b2);
+        fbits = PACKED ? pos_bits(fi, b1) : 0u;
       };
 
-      // lookup of x with the first two fingerprint matches checked at once (their keys are
-      // loaded together): slot s and counter word ce if hit; amb if neither matched and a third
-      // fingerprint match remains (the caller then runs `lookup`)
-      auto lookup2 = [&](KT x, bool act, uint32_t& s, uint32_t& ce, uint32_t& fi, uint32_t& fp,
-                         bool& hit, bool& amb) {
-        uint32_t b1, b2;
-        key_hash<ET>(en, x, seed, NB, b1, b2, fp);
-        ET e0, e1, e2, e3;
-        bool q0, q1, q2, q3;
-        if constexpr (sizeof(ET) == 2 && SB > 0) {  // a bucket word's two entries at once
-          const uint32_t v1 = reinterpret_cast<const uint32_t*>(T)[b1];
-          const uint32_t v2 = reinterpret_cast<const uint32_t*>(T)[b2];
-          e0 = (ET)v1;
-          e1 = (ET)(v1 >> 16);
-          e2 = (ET)v2;
-          e3 = (ET)(v2 >> 16);
-          const uint32_t fm = (en.fmask << en.sb) * 0x10001u;  // fingerprint fields
-          const uint32_t tg = (fp << en.sb) * 0x10001u;
-          const uint32_t d1 = (v1 ^ tg) & fm, d2 = (v2 ^ tg) & fm;
-          q0 = (d1 & 0xffffu) == 0;
-          q1 = (d1 >> 16) == 0;
-          q2 = (d2 & 0xffffu) == 0;
-          q3 = (d2 >> 16) == 0;
-        } else {
-          load_bucket(T, b1, e0, e1);
-          load_bucket(T, b2, e2, e3);
-          q0 = en.fp_eq(e0, fp);
-          q1 = en.fp_eq(e1, fp);
-          q2 = en.fp_eq(e2, fp);
-          q3 = en.fp_eq(e3, fp);
-        }
-        const ET r3 = q3 ? e3 : EMPTY;
-        const ET r23 = q2 ? e2 : r3;
-        const ET r123 = q1 ? e1 : r23;
-        const ET m1 = q0 ? e0 : r123;
-        const ET m2 = q0 ? r123 : (q1 ? r23 : (q2 ? r3 : EMPTY));
-        const uint32_t t1 = m1 == EMPTY ? 0u : en.slot(m1);
-        const uint32_t t2 = m2 == EMPTY ? 0u : en.slot(m2);
-        const KT k1 = keys[t1], k2 = keys[t2];
-        const uint32_t c1 = cw[t1], c2 = cw[t2];
-        const bool h1 = m1 != EMPTY && k1 == x;
-        const bool h2 = m2 != EMPTY && k2 == x;
-        hit = act && (h1 || h2);
-        s = h1 ? t1 : t2;
-        ce = h1 ? c1 : c2;
-        amb = act && !hit && (uint32_t)q0 + (uint32_t)q1 + (uint32_t)q2 + (uint32_t)q3 >= 3u;
-        fi = free_entry(e0, e1, e2, e3, b1, b2, fp >> 1);
-      };
-
-      uint32_t q = 0;  // items consumed
+      uint32_t q = 0;       // items consumed
       // The specialized kernel (SB > 0) keeps the ring position of item q, (roff + q) % RING,
-      // incrementally and compares both fingerprints of a bucket word at once (round 1: the same
-      // two changes measured 2-5 % slower in the runtime-layout kernel).
+      // incrementally and compares both fingerprints of a bucket word at once; the same two
+      // changes measured 2-5 % slower in the runtime-layout kernel (k = 2000), which keeps the
+      // modulo and the per-entry compares.
       uint32_t rq = roff;
       auto ring_at = [&](uint32_t lane_off) -> KT {
         if constexpr (SB > 0) {
@@ -622,8 +534,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const KT x = ring_at(lane);
         const uint32_t grp = __match_any_sync(PSS_FULL, x) & amask;
         int32_t s;
-        uint32_t ce, fi, fp;
-        lookup(x, act, s, ce, fi, fp);
+        uint32_t ce, fi, fp, fbits;
+        lookup(x, act, s, ce, fi, fp, fbits);
         const bool hit = s >= 0;
         const bool leader = act && (grp & ltm) == 0;
         const uint32_t missL = __ballot_sync(PSS_FULL, leader && !hit);
@@ -633,13 +545,13 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
         const bool inpre = leader && lane < c;
         const uint32_t mult = __popc(grp & pm);
-        if (inpre && hit) cw[s] = ce + mult;
+        if (inpre && hit) cnt[s] = ce + mult;
         const bool ins = inpre && !hit;
         const uint32_t v = size + __popc(missL & ltm);
         if (ins) {
           keys[v] = x;
-          cw[v] = PACKED ? (mult | (fi << cb)) : mult;
-          err[v] = (ERRT)0;
+          cnt[v] = mult | fbits;
+          if (!PACKED) err[v] = 0;
         }
         const uint32_t grow = __popc(missL & pm);
         insert_all(ins, x, v, fi, fp, size + grow);
@@ -649,285 +561,138 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         SS_STAT(1, c);
         __syncwarp();
       }
-      if (size == k) new_level(true);
+      if (size == k) new_level();
 
       // ---- all k counters occupied: misses evict the lowest slots of B_m (R1)
-      // A step takes a window of W = 32 R consecutive items, R rows of 32 (item p = 32 j + lane
-      // in row j), loaded by the previous step as soon as it knows its length.
-      constexpr uint32_t W = 32u * R;
-      static_assert(W <= ST, "a window spans at most two ring stages");
-      KT x[R];
-#pragma unroll
-      for (uint32_t j = 0; j < R; ++j) x[j] = 0;
-      auto next_window = [&]() {
-        if (q < L) {
-          ensure(q + min(W, L - q));
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) x[j] = ring_at(32u * j + lane);
-        }
-      };
-      next_window();
-      // one step; F: a full window (every step but the block's last), compiled separately so that
-      // the window-length predicates fold away
+#ifdef PSS_STATS
+      long long tk = 0, ph1 = 0, ph2 = 0, ph3 = 0, ph4 = 0, ph5 = 0;
+#endif
+      // one step; F: a full 32-item window (every step but the block's last), compiled separately
+      // so that the window-length predicates fold away
       auto full_step = [&](auto full) {
         constexpr bool F = decltype(full)::value;
-        const uint32_t nv = F ? W : min(W, L - q);
-        bool act[R];
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) act[j] = F || 32u * j + lane < nv;
+        const uint32_t nv = F ? 32u : min(32u, L - q);
+        ensure(q + nv);
+#ifdef PSS_STATS
+        tk = clock64();
+#endif
+        const bool act = F || lane < nv;
+        const uint32_t amask = F || nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
+        const KT x = ring_at(lane);
+        // the match is issued first and its result first used after the lookups, so that its
+        // latency (it grows with the number of distinct keys) overlaps them
+        const uint32_t grp_all = __match_any_sync(PSS_FULL, x);
 
-        // victim candidates (independent of the lookups): lane j of row r takes list entry
-        // cur + 32 r + lane; it is still in B_m iff its count is m. The valid ones are compacted
-        // into vic[] in list order: (slot | list index << 16, index entry).
-        uint32_t navail = 0;
-#pragma unroll
-        for (uint32_t r = 0; r < R; ++r) {
-          const uint32_t vi = cur + 32u * r + lane;
-          const bool inq = vi < vlen;
-          const uint32_t vs = inq ? (uint32_t)vq[vi] : 0u;
-          const uint32_t vc = cw[vs];
-          const bool valid = inq && (vc & CM) == m;
-          const uint32_t vmask = __ballot_sync(PSS_FULL, valid);
-          if (valid)
-            vic[navail + __popc(vmask & ltm)] =
-                make_uint2(vs | (vi << 16), PACKED ? vc >> cb : (uint32_t)pos[vs]);
-          navail += __popc(vmask);
-        }
-
-        // lookups of every row, then one test for the rare third fingerprint match
-        uint32_t s[R], ce[R], fi[R], fp[R];
-        bool hit[R];
-        bool amb = false;
-        if constexpr (R == 1) {  // one row: the first fingerprint match, rare re-checks inside
-          int32_t ss;
-          lookup(x[0], act[0], ss, ce[0], fi[0], fp[0]);
-          hit[0] = ss >= 0;
-          s[0] = hit[0] ? (uint32_t)ss : 0u;
+        // victims for this step (independent of the lookups): lane j holds the j-th next slot
+        // of B_m at or after the cursor (two bitmap words) and the index entry of its item
+        uint32_t w0 = cur >> 5;
+        uint32_t wa = bm[w0] & (0xffffffffu << (cur & 31u));
+        while (wa == 0) wa = bm[++w0];  // bmcount >= 1: some later word has a bit
+        const uint32_t wb = bm[w0 + 1];
+        const uint32_t ca = __popc(wa);
+        const uint32_t navail = min(32u, ca + __popc(wb));
+        const uint32_t ra = __popc(wa & ltm), rb = ca + __popc(wb & ltm);
+        if ((wa >> lane) & 1u) vic[ra] = w0 * 32 + lane;
+        if (((wb >> lane) & 1u) && rb < 32) vic[rb] = w0 * 32 + 32 + lane;
+        __syncwarp();
+        const uint32_t myvic = vic[lane];
+        uint32_t myop;
+        if (PACKED) {  // the victim's entry: its key's bucket pair and the position bits
+          const uint32_t tv = lane < navail ? myvic : 0;
+          const KT vk = keys[tv];
+          const uint32_t vc = cnt[tv];
+          uint32_t vb1, vb2, vfp;
+          key_hash<ET>(en, vk, seed, NB, vb1, vb2, vfp);
+          myop = 2 * ((vc >> 31) ? vb2 : vb1) + ((vc >> 30) & 1u);
         } else {
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) {
-            bool am;
-            lookup2(x[j], act[j], s[j], ce[j], fi[j], fp[j], hit[j], am);
-            amb |= am;
-          }
+          myop = pos[lane < navail ? myvic : 0];
         }
-        if (R > 1 && __ballot_sync(PSS_FULL, amb)) {
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) {
-            int32_t ss;
-            uint32_t c2, f2, p2;
-            lookup(x[j], act[j], ss, c2, f2, p2);  // the full check (every fingerprint match)
-            hit[j] = ss >= 0;
-            s[j] = hit[j] ? (uint32_t)ss : 0u;
-            ce[j] = c2;
-          }
-          SS_STAT(4, 1);
-        }
-        __syncwarp();  // vic[] written
 
-        // every miss is ranked in stream order (a key that misses twice is found below)
-        uint32_t missL[R], base[R];
-        uint32_t M = 0;
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          missL[j] = __ballot_sync(PSS_FULL, act[j] && !hit[j]);
-          base[j] = M;
-          M += __popc(missL[j]);
-        }
+        int32_t s;
+        uint32_t ce, fi, fp, fbits;
+        lookup(x, act, s, ce, fi, fp, fbits);
+        SS_TICK(ph2, tk, ce ^ (uint32_t)s ^ myop);
+        const uint32_t grp = grp_all & amask;
+        const bool hit = s >= 0;
+        const uint32_t cs = ce & CM;
+        const bool leader = act && (grp & ltm) == 0;
+        const uint32_t missL = __ballot_sync(PSS_FULL, leader && !hit);
+        const uint32_t rank = __popc(missL & ltm);
+        const uint32_t M = __popc(missL);
         const uint32_t Ms = min(M, navail);
+        const uint32_t vmax = __shfl_sync(PSS_FULL, myvic, (Ms ? Ms : 1) - 1);
         uint32_t c = nv;
-        if (M > navail) {  // the first miss without a fetched victim
-          uint32_t jr = 0;
-#pragma unroll
-          for (uint32_t j = 1; j < R; ++j)
-            if (base[j] <= navail) jr = j;
-          uint32_t mj = missL[0], bj = base[0];
-#pragma unroll
-          for (uint32_t j = 1; j < R; ++j)
-            if (jr == j) {
-              mj = missL[j];
-              bj = base[j];
-            }
-          c = 32u * jr + nth_set(mj, navail - bj);
+        if (Ms < M) {
+          c = nth_set(missL, Ms);  // no victim left for this miss
           SS_STAT(5, 1);
         }
-        // hazard: a victim slot whose item is also hit in the window. A hit slot with count m is
-        // at or after the cursor (every slot passed by the cursor was evicted or had left B_m),
-        // so it is among this step's victims iff it is <= the last one.
-        const uint32_t vmax = vic[Ms ? Ms - 1 : 0].x & 0xffffu;
-        bool conf = false;
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j)
-          conf |= hit[j] && Ms && (ce[j] & CM) == m && s[j] <= vmax;
+        // hazard: a victim slot whose item is also hit in the window
+        const bool conf = leader && hit && Ms && cs == m && (uint32_t)s <= vmax;
         if (__ballot_sync(PSS_FULL, conf)) {
-          uint32_t cpos = W;
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) {
-            if (hit[j] && Ms && (ce[j] & CM) == m && s[j] <= vmax) {
-              uint32_t rr = 0;  // s is victim rr, taken by the miss of rank rr
-              while ((vic[rr].x & 0xffffu) != s[j]) ++rr;
-              uint32_t jr = 0;
-#pragma unroll
-              for (uint32_t i = 1; i < R; ++i)
-                if (base[i] <= rr) jr = i;
-              uint32_t mm = 0, bb = 0;
-#pragma unroll
-              for (uint32_t i = 0; i < R; ++i)
-                if (jr == i) {
-                  mm = missL[i];
-                  bb = base[i];
-                }
-              for (uint32_t i = bb; i < rr; ++i) mm &= mm - 1u;
-              const uint32_t prr = 32u * jr + (uint32_t)(__ffs(mm) - 1);
-              // hit first (t < p): the hit is processed and the eviction waits; eviction first
-              // (t > p): the eviction is processed and the item at t becomes a miss
-              cpos = min(cpos, max(32u * j + lane, prr));
-            }
+          uint32_t cpos = 32;
+          if (conf) {
+            uint32_t rr = 0;
+            while (vic[rr] != (uint32_t)s) ++rr;
+            uint32_t mm = missL;
+            for (uint32_t i = 0; i < rr; ++i) mm &= mm - 1u;
+            const uint32_t pr = (uint32_t)(__ffs(mm) - 1);
+            cpos = max(lane, pr);
           }
           c = min(c, __reduce_min_sync(PSS_FULL, cpos));
           SS_STAT(6, 1);
         }
-        // Misses of [0, c) claim the free entry of their buckets for (fingerprint, victim slot)
-        // and read it back. Two misses of one key pick the same entry (same buckets, same
-        // snapshot): if every claim holds, no key misses twice in the window.
-        uint2 vv[R];
-        bool ev[R], won[R];
-        ET* tp[R];
-        ET mine[R];
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          const uint32_t rank = base[j] + __popc(missL[j] & ltm);
-          vv[j] = vic[min(rank, W - 1)];
-          vv[j].x &= 0xffffu;
-          ev[j] = act[j] && !hit[j] && 32u * j + lane < c;
-          const bool tryfi = ev[j] && fi[j] != 0xffffffffu;
-          mine[j] = en.make(fp[j], vv[j].x);
-          tp[j] = T + (tryfi ? fi[j] : 0u);
-          if (tryfi) *tp[j] = mine[j];
+        const uint32_t pm = c >= 32 ? PSS_FULL : ((1u << c) - 1u);
+        const bool inpre = leader && lane < c;
+        const uint32_t mult = __popc(grp & pm);
+        SS_TICK(ph3, tk, mult ^ vmax);
+        // hits: count += multiplicity; a hit counter leaves B_m
+        const bool hup = inpre && hit;
+        const bool hitm = hup && cs == m;
+        uint32_t* const cptr = cnt + (hit ? (uint32_t)s : 0u);
+        const uint32_t cnew = ce + mult;
+        if (hup) *cptr = cnew;
+        if (hitm) atomicAnd(&bm[(uint32_t)s >> 5], ~(1u << ((uint32_t)s & 31u)));
+        // misses: the victim takes the item, count m + multiplicity ("incremented by one" then
+        // further hits in the window), error m; its old item leaves the index
+        const bool ev = inpre && !hit;
+        const uint32_t v = __shfl_sync(PSS_FULL, myvic, rank & 31u);
+        const uint32_t op = __shfl_sync(PSS_FULL, myop, rank & 31u);
+        const uint32_t vnew = PACKED ? ((m + mult) | (m << cb) | fbits) : (m + mult);
+        ET* const tdel = T + op;
+        KT* const kptr = keys + v;
+        uint32_t* const vptr = cnt + v;
+        if (ev) {
+          *tdel = EMPTY;
+          *kptr = x;
+          *vptr = vnew;
+          if (!PACKED) err[v] = m;
         }
-        __syncwarp();
-        bool anylost = false;
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          won[j] = ev[j] && fi[j] != 0xffffffffu && *tp[j] == mine[j];
-          anylost |= ev[j] && !won[j];
-        }
-        const uint32_t lostb = __ballot_sync(PSS_FULL, anylost);
-        if (lostb) {
-          // a claim did not hold: two misses picked one entry (one key twice, or two keys
-          // sharing a bucket) or a miss found no free entry. Every key that misses more than once
-          // has a losing occurrence: for each losing miss, any other miss of its key ends the
-          // step before that key's second occurrence (which is a hit on the first one's slot).
-          uint32_t cd = c;
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) {
-            uint32_t lm = __ballot_sync(PSS_FULL, ev[j] && !won[j]);
-            while (lm) {
-              const uint32_t l = __ffs(lm) - 1;
-              lm &= lm - 1;
-              const KT xl = __shfl_sync(PSS_FULL, x[j], l);
-              uint32_t first = W, second = W;
-#pragma unroll
-              for (uint32_t i = 0; i < R; ++i) {
-                const uint32_t same = __ballot_sync(PSS_FULL, ev[i] && x[i] == xl);
-                if (same) {
-                  const uint32_t p0 = 32u * i + (uint32_t)(__ffs(same) - 1);
-                  const uint32_t rest = same & (same - 1);
-                  if (p0 < first) {
-                    second = first;
-                    first = p0;
-                  } else if (p0 < second) {
-                    second = p0;
-                  }
-                  if (rest) second = min(second, 32u * i + (uint32_t)(__ffs(rest) - 1));
-                }
-              }
-              cd = min(cd, second);
-            }
-          }
-          if (cd < c) {  // undo the claims at or after the new end; those before keep theirs
-            c = cd;
-#pragma unroll
-            for (uint32_t j = 0; j < R; ++j) {
-              const bool out = 32u * j + lane >= c;
-              if (won[j] && out) *tp[j] = EMPTY;
-              ev[j] = ev[j] && !out;
-              won[j] = won[j] && !out;
-            }
-            SS_STAT(13, 1);
-          }
-          __syncwarp();
-          SS_STAT(12, 1);
-        }
-        // hits: count + 1 per occurrence (occurrences of one key add to one counter; a hit
-        // counter at m leaves B_m and its list entry goes stale)
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j)
-          if (hit[j] && 32u * j + lane < c) atomicAdd(cw + s[j], 1u);
-        // misses: the victim takes the item, count m + 1 ("incremented by one"), error m; its old
-        // item leaves the index
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          ET* const tdel = T + vv[j].y;
-          KT* const kptr = keys + vv[j].x;
-          uint32_t* const vptr = cw + vv[j].x;
-          ERRT* const eptr = err + vv[j].x;
-          if (ev[j]) {
-            *tdel = EMPTY;
-            *kptr = x[j];
-            *vptr = PACKED ? ((m + 1u) | (fi[j] << cb)) : (m + 1u);
-            *eptr = (ERRT)m;
-            if (!PACKED) pos[vv[j].x] = (PT)fi[j];
-          }
-        }
-        if (lostb) {  // the misses whose claim did not hold insert serially (cuckoo kicks)
-          __syncwarp();
-#pragma unroll
-          for (uint32_t j = 0; j < R; ++j) {
-            uint32_t need = __ballot_sync(PSS_FULL, ev[j] && !won[j]);
-            SS_STAT(2, __popc(need));
-            bool failed = false;
-            while (need) {
-              const uint32_t l = __ffs(need) - 1;
-              uint32_t okl = 1;
-              if (lane == l) okl = slow_insert(x[j], vv[j].x);
-              failed |= __shfl_sync(PSS_FULL, okl, l) == 0;
-              __syncwarp();
-              need &= need - 1;
-            }
-            if (failed) {
-              SS_STAT(3, 1);
-              rehash(size);
-            }
-          }
-        }
-        uint32_t Mp = 0;
-#pragma unroll
-        for (uint32_t j = 0; j < R; ++j) {
-          const uint32_t pj = c >= 32u * (j + 1) ? PSS_FULL
-                              : (c <= 32u * j ? 0u : ((1u << (c - 32u * j)) - 1u));
-          Mp += __popc(missL[j] & pj);
-        }
-        // the cursor moves past the last victim taken (stale entries before it are skipped); a
-        // window of stale entries only is skipped as a whole
-        if (Mp)
-          cur = (vic[Mp - 1].x >> 16) + 1u;
-        else if (navail == 0)
-          cur = min(cur + W, vlen);
+        insert_all(ev, x, v, fi, fp, size);
+        SS_TICK(ph4, tk, v);
+        const uint32_t Mp = __popc(missL & pm);
+        const uint32_t last = __shfl_sync(PSS_FULL, myvic, (Mp ? Mp : 1) - 1);
+        if (Mp) cur = last + 1;
+        bmcount -= __popc(__ballot_sync(PSS_FULL, hitm)) + Mp;
         advance(c);
-        next_window();
         SS_STAT(0, 1);
         SS_STAT(9, Mp);
         SS_STAT(1, c);
-        if (vlen - cur < W && vscan < size) {
-          refill();
-          SS_STAT(11, 1);
+        if (bmcount == 0) {
+          SS_STAT(7, 1);
+          new_level();
         }
-        if (cur >= vlen && vscan >= size) new_level(false);
         __syncwarp();
+        SS_TICK(ph5, tk, bmcount);
       };
-      while (q + W <= L) full_step(std::true_type{});
+      while (q + 32 <= L) full_step(std::true_type{});
       while (q < L) full_step(std::false_type{});
+#ifdef PSS_STATS
+      SS_STAT(11, ph1);
+      SS_STAT(12, ph2);
+      SS_STAT(13, ph3);
+      SS_STAT(14, ph4);
+      SS_STAT(15, ph5);
+#endif
     }
 
     // ---- dump the leaf in slot order
@@ -935,9 +700,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     uint32_t* oc = a.counts + (size_t)r * k;
     uint32_t* oe = a.errs + (size_t)r * k;
     for (uint32_t t = lane; t < size; t += 32) {
+      const uint32_t ce = cnt[t];
       oi[t] = keys[t];
-      oc[t] = cw[t] & CM;
-      oe[t] = (uint32_t)err[t];
+      oc[t] = ce & CM;
+      oe[t] = PACKED ? (ce & ~POSM) >> cb : err[t];
     }
     if (lane == 0) a.sizes[r] = size;
     if (a.leaf_flags) {  // publish leaf r to the overlapping tree kernel
@@ -950,13 +716,8 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 }
 
 // ------------------------------------------------------------------------------ host side
-using SSKernel = void (*)(const SumArgs);
-
 struct SSPlan {
   bool gstate, packed;
-  int spec;   // 10: the kernel compiled for slot bits 10 / count bits 17
-  int errb;   // bytes per error
-  uint32_t R; // rows of 32 items per step
   uint32_t cb, sb, fmask;
   SSLayout L;
   size_t smem;
@@ -964,34 +725,9 @@ struct SSPlan {
   int slots;  // resident CTAs the device holds
 };
 
-template <typename KT>
-static SSKernel ss_kernel_of(bool gstate, bool packed, int spec, uint32_t R) {
-  if (gstate) return ss_summarize_kernel<KT, uint64_t, true, false, uint32_t>;
-  if (!packed) return ss_summarize_kernel<KT, uint16_t, false, false, uint32_t>;
-  if (spec == 10) {
-    if constexpr (sizeof(KT) == 4) {
-      if (R == 4) return ss_summarize_kernel<KT, uint16_t, false, true, uint8_t, 10, 17, 4>;
-    }
-    if (R == 2) return ss_summarize_kernel<KT, uint16_t, false, true, uint8_t, 10, 17, 2>;
-    return ss_summarize_kernel<KT, uint16_t, false, true, uint8_t, 10, 17, 1>;
-  }
-  return ss_summarize_kernel<KT, uint16_t, false, true, uint16_t>;
-}
-static SSKernel ss_kernel_of(int kb, const SSPlan& p) {
-  return kb == 4 ? ss_kernel_of<uint32_t>(p.gstate, p.packed, p.spec, p.R)
-                 : ss_kernel_of<uint64_t>(p.gstate, p.packed, p.spec, p.R);
-}
-
-// rows of 32 items per step of the specialized kernel (experiment hook PSS_SS_ROWS: 1, 2, 4)
-static uint32_t ss_rows(int kb) {
-  uint32_t R = 2;
-  if (const char* s = std::getenv("PSS_SS_ROWS")) R = (uint32_t)std::atoi(s);
-  if (R != 1 && R != 2 && R != 4) R = 2;
-  if (kb == 8 && R > 2) R = 2;  // a window spans at most two 64-key ring stages
-  return R;
-}
-
-static int ss_blocks_per_sm(SSKernel kern, size_t smem, const DevInfo& d) {
+template <typename KT, typename ET, bool G, bool PK>
+static int ss_blocks_per_sm(size_t smem, const DevInfo& d) {
+  auto kern = ss_summarize_kernel<KT, ET, G, PK>;
   if (smem > (size_t)d.smem_optin || allow_max_smem(kern, d) != cudaSuccess) return 0;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem) != cudaSuccess) {
@@ -1003,21 +739,17 @@ static int ss_blocks_per_sm(SSKernel kern, size_t smem, const DevInfo& d) {
 
 static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
   SSPlan p;
-  // counts <= Lmax need cb bits; the index position takes SS_PB bits above them when they fit
+  // count + error in one word: counts <= Lmax need cb bits, errors <= Lmax / k the rest
   const uint64_t Lmax = (n + P - 1) / P;
   p.cb = 1;
   while (p.cb < 32 && (1ull << p.cb) <= Lmax) ++p.cb;
-  p.packed = p.cb + SS_PB <= 32;
+  p.packed = p.cb < 30 && (Lmax / k) < (1ull << (30 - p.cb));  // bits 30-31: index position
   // 16-bit entries: the slot field's all-ones value must exceed k - 1
   uint32_t sb = 1;
   while ((1u << sb) - 1u < k) ++sb;
-  p.spec = p.packed && p.cb == 17 && sb == 10 ? 10 : 0;  // errors <= Lmax / k < 2^17 / 512
-  p.errb = p.spec ? 1 : (p.packed ? 2 : 4);               // packed: Lmax / k < 2^16
-  p.R = p.spec ? ss_rows(kb) : 1;
   const double dl = ss_debug_load();
-  uint32_t NB = ss_buckets(k, dl > 0 ? dl : ss_target_load());
-  if (p.packed) NB = std::min(NB, ((1u << SS_PB) - 1u) / 2u);  // packed words address < 2^SS_PB entries
-  SSLayout Ls = ss_layout(k, kb, 2, p.errb, p.packed, NB, p.R);
+  uint32_t NB = ss_buckets(k, dl > 0 ? dl : SS_LOAD);
+  SSLayout Ls = ss_layout(k, kb, 2, p.packed, NB);
   p.gstate = k > SS_K_SMALL || Ls.total > SS_SMEM_STATE_MAX;
   if (!p.gstate) {
     p.sb = sb;
@@ -1026,23 +758,27 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     if (const char* ps = std::getenv("PSS_DEBUG_SMEM_PAD"))  // experiment hook: fewer warps/SM
       pad = (size_t)std::atoll(ps);
     auto smem_of = [&](const SSLayout& L) { return SS_RING_BYTES + SS_BAR_BYTES + L.total + pad; };
-    const SSKernel kern = ss_kernel_of(kb, p);
-    const int nb = ss_blocks_per_sm(kern, smem_of(Ls), d);
+    auto blocks = [&](size_t smem) {
+      if (p.packed)
+        return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(smem, d)
+                       : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(smem, d);
+      return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(smem, d)
+                     : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem, d);
+    };
+    const int nb = blocks(smem_of(Ls));
     // The shared memory left over at this occupancy goes to the index: the largest bucket count
-    // that keeps `nb` warps per SM (fewer fingerprint collisions and serial inserts); packed
-    // counter words address at most 2^SS_PB entries.
-    const uint32_t nb_max = p.packed ? ((1u << SS_PB) - 1u) / 2u : 0x7fffffffu;
+    // that keeps `nb` warps per SM (fewer fingerprint collisions and serial inserts).
     if (dl == 0 && nb > 0) {
-      uint32_t lo = NB, hi = std::min(2 * NB, nb_max);
+      uint32_t lo = NB, hi = 2 * NB;
       while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) / 2;
-        if (ss_blocks_per_sm(kern, smem_of(ss_layout(k, kb, 2, p.errb, p.packed, mid, p.R)), d) >= nb)
+        if (blocks(smem_of(ss_layout(k, kb, 2, p.packed, mid))) >= nb)
           lo = mid;
         else
           hi = mid - 1;
       }
       NB = lo;
-      Ls = ss_layout(k, kb, 2, p.errb, p.packed, NB, p.R);
+      Ls = ss_layout(k, kb, 2, p.packed, NB);
     }
     p.L = Ls;
     p.smem = smem_of(Ls);
@@ -1050,12 +786,9 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     p.slots = (int)std::min<uint64_t>((uint64_t)nb * d.sms, 1u << 30);
   } else {
     p.packed = false;
-    p.spec = 0;
-    p.R = 1;
-    p.errb = 4;
     p.sb = 32;
     p.fmask = 0xffffffffu;
-    p.L = ss_layout(k, kb, 8, 4, false, ss_buckets(k, dl > 0 ? dl : 0.32), 1);
+    p.L = ss_layout(k, kb, 8, false, ss_buckets(k, dl > 0 ? dl : 0.32));
     p.smem = SS_RING_BYTES + SS_BAR_BYTES;
     p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
     p.slots = 8 * d.sms;
@@ -1101,10 +834,10 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.queue = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ws) + oq) + qi;
   a.gstate = p.gstate ? static_cast<unsigned char*>(ws) + og : nullptr;
   a.gstride = p.L.total;
-  a.o_cw = p.L.cw;
+  a.o_cnt = p.L.cnt;
   a.o_err = p.L.err;
   a.o_pos = p.L.pos;
-  a.o_vq = p.L.vq;
+  a.o_bm = p.L.bm;
   a.o_vic = p.L.vic;
   a.o_T = p.L.T;
   a.NB = p.L.NB;
@@ -1113,9 +846,38 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.fmask = p.fmask;
   cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  const SSKernel kern = ss_kernel_of(kb, p);
-  if (!p.gstate) allow_max_smem(kern, d);
-  kern<<<grid, 32, p.smem, s>>>(a);
+  if (!p.gstate) {
+    if (p.packed) {
+      // the common shape compiled with its layout constants: k in [512, 1023] (slot bits 10) and
+      // blocks of 2^16 .. 2^17 - 1 keys (count bits 17). (Slot bits 11, k in [1024, 2047], was
+      // measured too: 3 % faster on evicting inputs, 4-7 % slower on the fill-heavy C3 s >= 1.5.)
+      const int spec = p.cb == 17 && p.sb == 10 ? 10 : 0;
+      if (spec == 10)
+        allow_max_smem(kb == 4 ? ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17>
+                               : ss_summarize_kernel<uint64_t, uint16_t, false, true, 10, 17>, d);
+      if (kb == 4) {
+        if (spec == 10)
+          ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17><<<grid, 32, p.smem, s>>>(a);
+        else
+          ss_summarize_kernel<uint32_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
+      } else {
+        if (spec == 10)
+          ss_summarize_kernel<uint64_t, uint16_t, false, true, 10, 17><<<grid, 32, p.smem, s>>>(a);
+        else
+          ss_summarize_kernel<uint64_t, uint16_t, false, true><<<grid, 32, p.smem, s>>>(a);
+      }
+    } else {
+      if (kb == 4)
+        ss_summarize_kernel<uint32_t, uint16_t, false, false><<<grid, 32, p.smem, s>>>(a);
+      else
+        ss_summarize_kernel<uint64_t, uint16_t, false, false><<<grid, 32, p.smem, s>>>(a);
+    }
+  } else {
+    if (kb == 4)
+      ss_summarize_kernel<uint32_t, uint64_t, true, false><<<grid, 32, p.smem, s>>>(a);
+    else
+      ss_summarize_kernel<uint64_t, uint64_t, true, false><<<grid, 32, p.smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
