@@ -135,6 +135,76 @@ def leaves(A, k: int, P: int, which: Sequence[int] | None = None, threads: int =
         return list(ex.map(lambda r: space_saving(A, k, *rng[r]), idx))
 
 
+def leaves_padded(A, k: int, P: int, threads: int = 1):
+    """All P leaf summaries of Algorithm 1 (Space Saving per block) as padded
+    arrays: items/counts/errs [P, k] (uint64, zero beyond each leaf's size) and sizes [P] (uint32).
+    The same ``orc_space_saving`` as ``leaves``, written straight into each leaf's row; leaves
+    are independent, so they run on `threads` host threads (ctypes releases the GIL)."""
+    A, kb = _keys(A)
+    L = _load()
+    rng = bounds(A.size, P)
+    items, counts, errs = (np.zeros((P, max(k, 1)), np.uint64) for _ in range(3))
+    sizes = np.zeros(P, np.uint32)
+    base = A.ctypes.data if A.size else None
+    row = max(k, 1) * 8
+
+    def one(r):
+        lo, hi = rng[r]
+        sizes[r] = L.orc_space_saving(base, kb, lo, hi, k, items.ctypes.data + r * row,
+                                      counts.ctypes.data + r * row, errs.ctypes.data + r * row)
+
+    if threads <= 1:
+        for r in range(P):
+            one(r)
+    else:
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(P)))
+    return items, counts, errs, sizes
+
+
+def tree_padded(items, counts, errs, sizes, k: int, threads: int = 1) -> Summary:
+    """ParallelReduction with COMBINE over the fixed binary tree (Alg. 1 line 7; reading R6) on
+    padded [P, k] leaves, level by level exactly as ``orc_tree``: nodes (2i, 2i+1) of a level are
+    merged by ``orc_combine`` (Algorithm 2), an odd last node is carried up unchanged, the root is
+    put in canonical order (R5). The COMBINEs of one level are independent and run on `threads`
+    host threads; the tree's shape and every COMBINE's arithmetic are ``orc_tree``'s."""
+    L = _load()
+    P = sizes.size
+    if P == 0:
+        return empty_summary()
+    ci, cc, ce = (np.ascontiguousarray(a, dtype=np.uint64) for a in (items, counts, errs))
+    cs = np.ascontiguousarray(sizes, dtype=np.uint32).copy()
+    kk = ci.shape[1]
+    row = kk * 8
+    while cs.size > 1:
+        cur = cs.size
+        nxt = (cur + 1) // 2
+        ni, nn, ne = (np.zeros((nxt, kk), np.uint64) for _ in range(3))
+        ns = np.zeros(nxt, np.uint32)
+
+        def one(i):
+            a, b = 2 * i, 2 * i + 1
+            ns[i] = L.orc_combine(ci.ctypes.data + a * row, cc.ctypes.data + a * row,
+                                  ce.ctypes.data + a * row, int(cs[a]),
+                                  ci.ctypes.data + b * row, cc.ctypes.data + b * row,
+                                  ce.ctypes.data + b * row, int(cs[b]), k,
+                                  ni.ctypes.data + i * row, nn.ctypes.data + i * row,
+                                  ne.ctypes.data + i * row)
+
+        if threads <= 1 or cur // 2 < 2:
+            for i in range(cur // 2):
+                one(i)
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(cur // 2)))
+        if cur & 1:  # odd last node carried up unchanged
+            ni[nxt - 1], nn[nxt - 1], ne[nxt - 1] = ci[cur - 1], cc[cur - 1], ce[cur - 1]
+            ns[nxt - 1] = cs[cur - 1]
+        ci, cc, ce, cs = ni, nn, ne, ns
+    n0 = int(cs[0])
+    return canonical(Summary(ci[0, :n0].copy(), cc[0, :n0].copy(), ce[0, :n0].copy()))
+
+
 def min_count(S, k: int) -> int:
     """MIN(S), Alg. 2 lines 2-3, reading R4 (0 unless all k counters used)."""
     S = _summary(S)

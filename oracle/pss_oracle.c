@@ -45,6 +45,11 @@ void orc_bounds(uint64_t n, uint32_t p, uint32_t r, uint64_t* lo, uint64_t* hi) 
  *   R3: err = 0 on fill, err = m (the evicted minimum) on eviction (Metwally's epsilon).
  * Output: slots 0..size-1 in slot order. Returns size.
  */
+/* Compiled twice by gcc (AVX2 and baseline x86-64, chosen at load time) only so that the full-size
+ * parity tests finish in minutes; the C below is the same for both. */
+#if defined(__GNUC__) && defined(__x86_64__) && !defined(__clang__)
+__attribute__((target_clones("arch=x86-64-v3", "default")))
+#endif
 uint32_t orc_space_saving(const void* A, int key_bytes, uint64_t lo, uint64_t hi, uint32_t k,
                           uint64_t* items, uint64_t* counts, uint64_t* errs) {
   uint32_t size = 0;

@@ -2,9 +2,9 @@
 
 All arithmetic is integer, so the bar is bit-exact: leaves in slot order, merged summaries and
 the root in canonical order, candidates in root order, exact counts, and the final answer.
-Small cases compare every output; full BASELINE sizes (in bench.py's launch configuration)
-compare sampled leaves one by one plus properties that hold at any size, and the final answer
-against a brute-force histogram.
+Small cases and the full BASELINE sizes (in bench.py's launch configuration) compare every
+output: every leaf, the root, candidates, exact counts and the answer (the last also against a
+brute-force histogram).
 """
 import numpy as np
 import pytest
@@ -277,14 +277,25 @@ FULL = ["C1", "C2", "H", "C3-s0.5", "C3-s1.0", "C3-s1.5", "C3-s2.0", "C3-s3.0", 
         "C4-k1000", "C4-k5000", "C4-k20000", "C5"]
 
 
+def padded_host(S):
+    """Device summaries -> numpy (sizes, items, counts, errs) with zeros beyond each size."""
+    sz = S.sizes.cpu().numpy().astype(np.int64)
+    mask = np.arange(S.k)[None, :] < sz[:, None]
+    out = [sz]
+    for t in (S.items, S.counts, S.errs):
+        out.append(np.where(mask, t.cpu().numpy().astype(np.uint64), np.uint64(0)))
+    return out
+
+
 @pytest.mark.parametrize("name", FULL)
 def test_full_size(pss, name):
-    """BASELINE.json configs at full size, bench.py's launch configuration (k, P): sampled leaves
-    bit-exact; root guarantees (f <= f_hat <= f + err, err <= n/k, no false negatives, sum <= n)
-    with exact f from the oracle's verification; candidates, exact counts and the answer exact;
-    the answer equals the brute-force k-majority set."""
+    """BASELINE.json configs at full size, bench.py's launch configuration (k, P): EVERY leaf
+    (slot order) and the root (canonical order) bit-exact against the oracle (Space Saving per
+    block; the fixed COMBINE tree), both from
+    the separate calls and from the fused pss_summarize_merge; candidates, exact counts and the
+    answer exact; the answer equals the brute-force k-majority set (recall 1)."""
     w = inputs.WORKLOADS[name]
-    need = w.n * w.key_bytes * 4
+    need = w.n * w.key_bytes * 4 + w.P * w.k * 8 * 6
     try:
         import psutil
         if psutil.virtual_memory().available < need + (8 << 30):
@@ -294,28 +305,24 @@ def test_full_size(pss, name):
     A = w.generate()
     n, k, P = A.size, w.k, w.P
     got = run_path(pss, A, k, P)
-    sample = sorted({0, 1, P // 3, P // 2, P - 2, P - 1} | set(range(7, P, max(1, P // 6))))
-    ref_leaves = oracle.leaves(A, k, P, which=sample, threads=inputs.host_threads())
-    for r, ref in zip(sample, ref_leaves):
-        assert got["leaves"].host(r) == ref.as_tuples(), f"{name} leaf {r}"
-    root = got["root"].host(0)
-    assert got["f_root"].host(0) == root  # pss_summarize_merge = pss_summarize + pss_merge
-    for r in sample:
-        assert got["f_leaves"].host(r) == got["leaves"].host(r)
-    items = np.array([x for x, _, _ in root], dtype=np.uint64)
-    f = oracle.verify(A, items).tolist()
-    assert len(root) <= k and sum(c for _, c, _ in root) <= n
-    keyed = [(-c, x) for x, c, _ in root]
-    assert keyed == sorted(keyed)  # canonical order
-    for (x, c, e), fx in zip(root, f):
-        assert fx <= c <= fx + e and e <= n // k
+    th = inputs.host_threads()
+    it, c, e, sz = oracle.leaves_padded(A, k, P, threads=th)
+    for which in ("leaves", "f_leaves"):
+        gsz, git, gc, ge = padded_host(got[which])
+        bad = np.flatnonzero((gsz != sz) | (git != it).any(1) | (gc != c).any(1) | (ge != e).any(1))
+        assert bad.size == 0, f"{name}: {bad.size} of {P} leaves differ ({which}), first {bad[:5]}"
+    root = oracle.tree_padded(it, c, e, sz, k, threads=th)
+    del it, c, e
+    assert got["root"].host(0) == root.as_tuples(), f"{name} root"
+    assert got["f_root"].host(0) == root.as_tuples(), f"{name} root (pss_summarize_merge)"
     thr = oracle.threshold(n, k)
-    assert got["cand"] == [x for x, c, _ in root if c >= thr]
+    assert got["cand"] == oracle.prune(root, n, k).tolist()
+    assert got["cand"] == [int(x) for x, cc in zip(root.items, root.counts) if cc >= thr]
     assert got["exact"] == oracle.verify(A, np.array(got["cand"], np.uint64)).tolist()
     want = bruteforce_kmajority(A, k)
     assert got["result"] == want
     assert got["exact_km"] == want
-    assert set(want[0]) <= set(items.tolist())  # recall 1
+    assert set(want[0]) <= set(root.items.tolist())  # recall 1
 
 
 @pytest.mark.parametrize("load", [0.75, 0.85])

@@ -471,3 +471,26 @@ def test_stream_binary_counter_equals_fixed_tree():
         if c == 1:
             acc = oracle.canonical(acc)
         assert acc.as_tuples() == oracle.tree(leaves[:c], k).as_tuples(), c
+
+
+# ---------------------------------------------------------------- full-size helpers (threaded)
+@pytest.mark.parametrize("n,P,kb", [(50_000, 1, 4), (50_000, 2, 4), (50_000, 7, 8), (30_001, 13, 4),
+                                    (5, 9, 4), (0, 3, 4), (70_000, 64, 8)])
+def test_padded_leaves_and_parallel_tree_equal_the_sequential_ones(n, P, kb):
+    """leaves_padded / tree_padded (the threaded forms the full-size GPU parity tests use) equal
+    leaves / orc_tree computed one COMBINE at a time, for odd level sizes (the carried node, R6),
+    empty leaves (P > n) and both key widths. Pinned to the sequential oracle, itself pinned above
+    by the worked examples, closed forms and exhaustive guarantees."""
+    rng = np.random.default_rng(n + P)
+    dt = np.uint32 if kb == 4 else np.uint64
+    A = (rng.zipf(1.3, size=n) % 5000).astype(dt) * dt(2654435761 & 0xFFFFFFFF)
+    for k in (2, 17, 100):
+        ref = oracle.leaves(A, k, P)
+        it, c, e, sz = oracle.leaves_padded(A, k, P, threads=4)
+        assert sz.tolist() == [len(s) for s in ref]
+        for r in range(P):
+            got = oracle.Summary(it[r, :sz[r]], c[r, :sz[r]], e[r, :sz[r]])
+            assert got.as_tuples() == ref[r].as_tuples()
+            assert not it[r, sz[r]:].any() and not c[r, sz[r]:].any()
+        assert oracle.tree_padded(it, c, e, sz, k, threads=4).as_tuples() == \
+            oracle.tree(ref, k).as_tuples()
