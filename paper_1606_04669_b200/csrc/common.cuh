@@ -160,6 +160,13 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0 = 0,
                              uint32_t r1 = 0xffffffffu, uint32_t qi = 0, uint32_t T = 1,
                              uint32_t* leaf_flags = nullptr, bool pdl = false);
+// K1h (hist.cu): leaves of blocks with at most k distinct keys as exact histograms; the other
+// leaves are flagged (flagged[r] = 1) for K1
+bool hist_used(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d);
+cudaError_t hist_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P, void* items,
+                        uint32_t* counts, uint32_t* errs, uint32_t* sizes, uint32_t* queue,
+                        unsigned char* flagged, cudaStream_t s, const DevInfo& d, uint32_t r0,
+                        uint32_t r1, uint32_t T, uint32_t* leaf_flags);
 // partition queues in the summarize workspace: launches over disjoint ranges [r0, r1) that may be
 // in flight together use distinct qi < SS_MAX_RANGES
 constexpr uint32_t SS_MAX_RANGES = 64;

@@ -475,7 +475,6 @@ __device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
   KT* const xlo = sm.xlo;
   uint32_t* const red = sm.red;
   uint32_t* const hist = sm.hist;
-  const uint32_t H2 = 1u << a.logH2, hmask = H2 - 1u;
   (void)NP;
   (void)xhi;
   const uint32_t n1 = ldx<CG>(ina.sizes + li);
@@ -499,6 +498,11 @@ __device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
   const KT* i2 = has_r ? reinterpret_cast<const KT*>(inb.items) + (size_t)ri * k : nullptr;
   const uint32_t* c2 = has_r ? inb.counts + (size_t)ri * k : nullptr;
   const uint32_t* e2 = has_r ? inb.errs + (size_t)ri * k : nullptr;
+  // S2's index: sized from S2's actual size (load <= 1/2), at most the planned capacity, so that
+  // unfull summaries (large k) clear and probe a table of their own size
+  uint32_t lh = 5;
+  while (lh < a.logH2 && (1u << lh) < 2u * n2) ++lh;
+  const uint32_t H2 = 1u << lh, hmask = H2 - 1u;
 
   // stage S1 -> u[0, n1), S2 -> u[n1, n1 + n2); minima (Alg. 2 l.2-3, R4). The loads of
   // both summaries are issued before their stores.
@@ -551,7 +555,7 @@ __device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
   m_tick(0, lv);
   // index S2's items (Find of Alg. 2 l.5)
   for (uint32_t t = tid; t < n2; t += NT) {
-    uint32_t h = hslot(ukey[n1 + t], a.logH2);
+    uint32_t h = hslot(ukey[n1 + t], lh);
     while (atomicCAS(&ht[h], 0xffffffffu, t) != 0xffffffffu) h = (h + 1u) & hmask;
   }
   __syncthreads();
@@ -559,7 +563,7 @@ __device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
   // counters of S1: matched -> f1 + f2 and Remove from S2; else f1 + m2 (Alg. 2 l.4-13)
   for (uint32_t t = tid; t < n1; t += NT) {
     const KT x = ukey[t];
-    uint32_t h = hslot(x, a.logH2);
+    uint32_t h = hslot(x, lh);
     uint32_t j;
     while ((j = ht[h]) != 0xffffffffu && ukey[n1 + j] != x) h = (h + 1u) & hmask;
     if (j != 0xffffffffu) {

@@ -199,6 +199,7 @@ struct SumArgs {
   uint32_t* errs;
   uint32_t* sizes;
   uint32_t* queue;
+  const unsigned char* skip;  // non-null: only leaves r with skip[r] != 0 (flagged by hist.cu)
   unsigned char* gstate;  // per-CTA state when it does not fit shared memory
   size_t gstride;
   size_t o_cnt, o_err, o_pos, o_bm, o_vic, o_T;
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     if (lane == 0) r = a.r0 + atomicAdd(a.queue, 1u);
     r = __shfl_sync(PSS_FULL, r, 0);
     if (r >= a.r1) break;
+    if (a.skip && !a.skip[r]) continue;  // leaf written by the histogram kernel (hist.cu)
     uint64_t lo, hi;
     if (a.T <= 1) {
       lo = (uint64_t)r * n / P;  // Alg. 1 l.3-4: r*n < 2^63 as n <= 2^31
@@ -797,12 +799,24 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   return p;
 }
 
-size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
-  SSPlan p = ss_plan(n, kb, k, P, d);
+// workspace: K1's partition queues, the histogram kernel's queues and per-leaf flags, K1's
+// global-memory states (large k)
+struct SumWs {
+  size_t q, hq, flagged, g, total;
+};
+static SumWs sum_ws(const SSPlan& p, uint32_t P) {
+  SumWs w;
   Bump b;
-  b.take<uint32_t>(SS_MAX_RANGES);
-  if (p.gstate) b.take<unsigned char>(p.L.total * (size_t)p.grid);
-  return b.bytes();
+  w.q = b.take<uint32_t>(SS_MAX_RANGES);
+  w.hq = b.take<uint32_t>(SS_MAX_RANGES);
+  w.flagged = b.take<unsigned char>(P);
+  w.g = p.gstate ? b.take<unsigned char>(p.L.total * (size_t)p.grid) : 0;
+  w.total = b.bytes();
+  return w;
+}
+
+size_t summarize_ws(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+  return sum_ws(ss_plan(n, kb, k, P, d), P).total;
 }
 
 cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t P,
@@ -814,10 +828,18 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   if (r1 > P) r1 = P;
   if (r0 >= r1 || qi >= SS_MAX_RANGES) return cudaErrorInvalidValue;
   const int grid = (int)std::min<uint64_t>(r1 - r0, (uint64_t)p.grid);
-  Bump b;
-  const size_t oq = b.take<uint32_t>(SS_MAX_RANGES);
-  const size_t og = p.gstate ? b.take<unsigned char>(p.L.total * (size_t)p.grid) : 0;
+  const SumWs W = sum_ws(p, P);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  // blocks with at most k distinct keys: the histogram kernel; K1 takes the others
+  const bool hist = hist_used(n, kb, k, P, d);
+  if (hist) {
+    cudaError_t e = hist_launch(A, n, kb, k, P, items, counts, errs, sizes,
+                                reinterpret_cast<uint32_t*>(w + W.hq) + qi, w + W.flagged, s, d,
+                                r0, r1, T, leaf_flags);
+    if (e != cudaSuccess) return e;
+  }
   SumArgs a;
+  a.skip = hist ? w + W.flagged : nullptr;
   a.A = A;
   a.n = n;
   a.k = k;
@@ -831,8 +853,8 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.counts = counts;
   a.errs = errs;
   a.sizes = sizes;
-  a.queue = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ws) + oq) + qi;
-  a.gstate = p.gstate ? static_cast<unsigned char*>(ws) + og : nullptr;
+  a.queue = reinterpret_cast<uint32_t*>(w + W.q) + qi;
+  a.gstate = p.gstate ? w + W.g : nullptr;
   a.gstride = p.L.total;
   a.o_cnt = p.L.cnt;
   a.o_err = p.L.err;
