@@ -55,7 +55,9 @@ typedef enum {
   PSS_OP_VERIFY = 3,
   PSS_OP_QUERY = 4,
   PSS_OP_EXACT = 5, /* pss_exact_kmajority; P is ignored */
-  PSS_OP_SUMMARIZE_MERGE = 6
+  PSS_OP_SUMMARIZE_MERGE = 6,
+  PSS_OP_COMBINE_WIDE = 7, /* pss_combine_wide; P = count */
+  PSS_OP_MERGE_WIDE = 8    /* pss_merge_wide; P = count; n is ignored */
 } pss_op;
 
 #define PSS_MAX_K 65000u
@@ -140,6 +142,45 @@ pss_status pss_combine(const pss_summaries* a, const pss_summaries* b, pss_summa
  */
 pss_status pss_prune(const pss_summaries* root, uint64_t n, void* d_cand, uint32_t* d_n_cand,
                      cudaStream_t stream);
+
+/*
+ * Wide summaries: the same counters with uint64 f_hat and eps, for the tree above the leaves when
+ * the summarized stream may exceed 2^31 items -- the top levels over several ranks' subtree roots
+ * (the paper's MPI reduction) and the on-line stream's upper tree (P:195
+ * streams of 29 10^9 items; R14). Reading R9 bounds a u32 count by n + n/k < 2^32 only for
+ * n <= 2^31; with 64-bit counters the bound is n <= 2^63. Layout and order as pss_summaries.
+ */
+typedef struct {
+  int32_t key_type;  /* pss_key_type */
+  uint32_t k;        /* counters per summary, 2 <= k <= PSS_MAX_K */
+  uint32_t count;    /* number of summaries */
+  void* items;       /* [count][k] uint32_t or uint64_t */
+  uint64_t* counts;  /* [count][k] f_hat */
+  uint64_t* errs;    /* [count][k] eps */
+  uint32_t* sizes;   /* [count] occupied counters, <= k */
+} pss_wsummaries;
+
+/* pss_widen -- out[i] = in[i] with 64-bit counts and errors (same k, key type and count; same
+ * order). No workspace. */
+pss_status pss_widen(const pss_summaries* in, pss_wsummaries* out, cudaStream_t stream);
+
+/* pss_combine_wide -- out[i] = COMBINE(a[i], b[i]) (Alg. 2; R3-R5) with 64-bit
+ * arithmetic, canonical order. workspace: pss_workspace_bytes(PSS_OP_COMBINE_WIDE, 0, k, count,
+ * kt). */
+pss_status pss_combine_wide(const pss_wsummaries* a, const pss_wsummaries* b,
+                            pss_wsummaries* out, void* d_ws, size_t ws_bytes,
+                            cudaStream_t stream);
+
+/* pss_merge_wide -- the fixed binary tree (R6, Alg. 1 l.7) over nodes->count wide summaries (e.g.
+ * the ranks' subtree roots in rank order): the root in canonical order (a single summary is put in
+ * canonical order). workspace: pss_workspace_bytes(PSS_OP_MERGE_WIDE, 0, k, count, kt). */
+pss_status pss_merge_wide(const pss_wsummaries* nodes, pss_wsummaries* root, void* d_ws,
+                          size_t ws_bytes, cudaStream_t stream);
+
+/* pss_prune_wide -- pss_prune on a wide root: counters with f_hat >= floor(n/k) + 1 (R7),
+ * root order, for any n < 2^63. */
+pss_status pss_prune_wide(const pss_wsummaries* root, uint64_t n, void* d_cand,
+                          uint32_t* d_n_cand, cudaStream_t stream);
 
 /*
  * pss_verify -- the off-line verification scan ("a parallel scan of the input can be used to

@@ -29,11 +29,13 @@ lib_path = os.environ.get("PSS_LIB") or os.path.join(_PKG, "libpss.so")  # PSS_L
 KEY_U32, KEY_U64 = 0, 1
 OP_SUMMARIZE, OP_MERGE, OP_COMBINE, OP_VERIFY, OP_QUERY = range(5)
 OP_SUMMARIZE_MERGE = 6
+OP_COMBINE_WIDE, OP_MERGE_WIDE = 7, 8
 STATUS = {0: "PSS_OK", 1: "PSS_ERR_INVALID_ARG", 2: "PSS_ERR_UNSUPPORTED",
           3: "PSS_ERR_CAPACITY_MISMATCH", 4: "PSS_ERR_WORKSPACE_TOO_SMALL", 5: "PSS_ERR_CUDA"}
 EXPORTED_SYMBOLS = ["pss_workspace_bytes", "pss_summarize", "pss_summarize_merge", "pss_merge",
                     "pss_combine",
                     "pss_prune", "pss_verify", "pss_report", "pss_query", "pss_query_host",
+                    "pss_widen", "pss_combine_wide", "pss_merge_wide", "pss_prune_wide",
                     "pss_status_string", "pss_version"]
 
 
@@ -67,8 +69,14 @@ _lib.pss_verify.argtypes = [_vp, _u64, _i32, _vp, _u32, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_report.argtypes = [_vp, _u32, _vp, _vp, _i32, _u64, _u32, _vp, _vp, _vp, _vp]
 _lib.pss_query.argtypes = [_vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
 _lib.pss_query_host.argtypes = [_vp, _vp, _u64, _i32, _u32, _u32, _vp, _vp, _vp, _vp, _sz, _vp]
+# wide summaries (include/pss.h pss_wsummaries) share pss_summaries' layout: 64-bit counts/errs
+_lib.pss_widen.argtypes = [_SP, _SP, _vp]
+_lib.pss_combine_wide.argtypes = [_SP, _SP, _SP, _vp, _sz, _vp]
+_lib.pss_merge_wide.argtypes = [_SP, _SP, _vp, _sz, _vp]
+_lib.pss_prune_wide.argtypes = [_SP, _u64, _vp, _vp, _vp]
 for _f in ("pss_summarize", "pss_summarize_merge", "pss_merge", "pss_combine", "pss_prune",
-           "pss_verify", "pss_report", "pss_query", "pss_query_host"):
+           "pss_verify", "pss_report", "pss_query", "pss_query_host", "pss_widen",
+           "pss_combine_wide", "pss_merge_wide", "pss_prune_wide"):
     getattr(_lib, _f).restype = _i32
 _lib.pss_status_string.argtypes = [_i32]
 _lib.pss_status_string.restype = ctypes.c_char_p
@@ -109,10 +117,16 @@ def _dev_keys(A: torch.Tensor) -> torch.Tensor:
     return A
 
 
-def _ws(nbytes: int, ws: torch.Tensor | None, device) -> torch.Tensor:
+def _ws(nbytes: int, ws: torch.Tensor | None, device, stream=None) -> torch.Tensor:
+    """The caller's workspace if large enough, else a temporary. A temporary is marked as in use
+    on `stream` (record_stream): the call only enqueues work, so without it the caching
+    allocator could hand the block to a new allocation while the kernels still use it."""
     if ws is not None and ws.numel() * ws.element_size() >= nbytes:
         return ws.view(torch.uint8) if ws.dtype != torch.uint8 else ws
-    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    if stream is not None:
+        t.record_stream(stream)
+    return t
 
 
 def pss_workspace_bytes(op: int, n: int, k: int, P: int, key_type: int) -> int:
@@ -128,11 +142,17 @@ class Summaries:
     sizes: torch.Tensor   # [count] uint32
 
     @staticmethod
-    def empty(count: int, k: int, key_type: int, device="cuda") -> "Summaries":
+    def empty(count: int, k: int, key_type: int, device="cuda", wide: bool = False) -> "Summaries":
+        """wide: 64-bit counts and errors (pss_wsummaries, the tree above the leaves)."""
+        ct = torch.uint64 if wide else torch.uint32
         return Summaries(torch.empty((count, k), dtype=_key_dtype(key_type), device=device),
-                         torch.empty((count, k), dtype=torch.uint32, device=device),
-                         torch.empty((count, k), dtype=torch.uint32, device=device),
+                         torch.empty((count, k), dtype=ct, device=device),
+                         torch.empty((count, k), dtype=ct, device=device),
                          torch.zeros((count,), dtype=torch.uint32, device=device))
+
+    @property
+    def wide(self) -> bool:
+        return self.counts.dtype == torch.uint64
 
     @property
     def k(self) -> int:
@@ -165,7 +185,7 @@ def pss_summarize(A: torch.Tensor, k: int, P: int, out: Summaries | None = None,
     A = _dev_keys(A)
     kt = _key_type(A)
     out = out or Summaries.empty(P, k, kt, A.device)
-    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE, A.numel(), k, P, kt), workspace, A.device)
+    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE, A.numel(), k, P, kt), workspace, A.device, stream)
     c = out._c()
     _check("pss_summarize", _lib.pss_summarize(A.data_ptr(), A.numel(), kt, k, P, ctypes.byref(c),
                                                ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -180,7 +200,7 @@ def pss_summarize_merge(A: torch.Tensor, k: int, P: int, leaves: Summaries | Non
     kt = _key_type(A)
     leaves = leaves or Summaries.empty(P, k, kt, A.device)
     root = root or Summaries.empty(1, k, kt, A.device)
-    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE_MERGE, A.numel(), k, P, kt), workspace, A.device)
+    ws = _ws(pss_workspace_bytes(OP_SUMMARIZE_MERGE, A.numel(), k, P, kt), workspace, A.device, stream)
     a, b = leaves._c(), root._c()
     _check("pss_summarize_merge", _lib.pss_summarize_merge(
         A.data_ptr(), A.numel(), kt, k, P, ctypes.byref(a), ctypes.byref(b), ws.data_ptr(),
@@ -193,7 +213,7 @@ def pss_merge(leaves: Summaries, out: Summaries | None = None,
     """Fixed binary COMBINE tree over the leaves (Alg. 1 l.7, Alg. 2) -> root (canonical)."""
     out = out or Summaries.empty(1, leaves.k, leaves.key_type, leaves.items.device)
     ws = _ws(pss_workspace_bytes(OP_MERGE, 0, leaves.k, leaves.count, leaves.key_type), workspace,
-             leaves.items.device)
+             leaves.items.device, stream)
     a, b = leaves._c(), out._c()
     _check("pss_merge", _lib.pss_merge(ctypes.byref(a), ctypes.byref(b), ws.data_ptr(), ws.numel(),
                                        _stream(stream)))
@@ -204,11 +224,66 @@ def pss_combine(a: Summaries, b: Summaries, out: Summaries | None = None,
                 workspace: torch.Tensor | None = None, stream=None) -> Summaries:
     """out[i] = COMBINE(a[i], b[i]) (Alg. 2), canonical order."""
     out = out or Summaries.empty(a.count, a.k, a.key_type, a.items.device)
-    ws = _ws(pss_workspace_bytes(OP_COMBINE, 0, a.k, a.count, a.key_type), workspace, a.items.device)
+    ws = _ws(pss_workspace_bytes(OP_COMBINE, 0, a.k, a.count, a.key_type), workspace, a.items.device, stream)
     ca, cb, co = a._c(), b._c(), out._c()
     _check("pss_combine", _lib.pss_combine(ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co),
                                            ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
+
+
+def _need(S: Summaries, wide: bool, fn: str):
+    if S.wide != wide:
+        raise TypeError(f"{fn}: {'wide' if wide else 'narrow'} summaries expected")
+
+
+def pss_widen(S: Summaries, out: Summaries | None = None, stream=None) -> Summaries:
+    """The same summaries with 64-bit counts and errors (include/pss.h pss_widen)."""
+    _need(S, False, "pss_widen")
+    out = out or Summaries.empty(S.count, S.k, S.key_type, S.items.device, wide=True)
+    a, b = S._c(), out._c()
+    _check("pss_widen", _lib.pss_widen(ctypes.byref(a), ctypes.byref(b), _stream(stream)))
+    return out
+
+
+def pss_combine_wide(a: Summaries, b: Summaries, out: Summaries | None = None,
+                     workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """out[i] = COMBINE(a[i], b[i]) (Alg. 2) with 64-bit counts, canonical order."""
+    _need(a, True, "pss_combine_wide")
+    out = out or Summaries.empty(a.count, a.k, a.key_type, a.items.device, wide=True)
+    ws = _ws(pss_workspace_bytes(OP_COMBINE_WIDE, 0, a.k, a.count, a.key_type), workspace,
+             a.items.device, stream)
+    ca, cb, co = a._c(), b._c(), out._c()
+    _check("pss_combine_wide", _lib.pss_combine_wide(ctypes.byref(ca), ctypes.byref(cb),
+                                                     ctypes.byref(co), ws.data_ptr(), ws.numel(),
+                                                     _stream(stream)))
+    return out
+
+
+def pss_merge_wide(nodes: Summaries, out: Summaries | None = None,
+                   workspace: torch.Tensor | None = None, stream=None) -> Summaries:
+    """The fixed binary tree (R6) over wide summaries -> wide root (canonical)."""
+    _need(nodes, True, "pss_merge_wide")
+    out = out or Summaries.empty(1, nodes.k, nodes.key_type, nodes.items.device, wide=True)
+    ws = _ws(pss_workspace_bytes(OP_MERGE_WIDE, 0, nodes.k, nodes.count, nodes.key_type),
+             workspace, nodes.items.device, stream)
+    a, b = nodes._c(), out._c()
+    _check("pss_merge_wide", _lib.pss_merge_wide(ctypes.byref(a), ctypes.byref(b), ws.data_ptr(),
+                                                 ws.numel(), _stream(stream)))
+    return out
+
+
+def pss_prune_wide(root: Summaries, n: int, stream=None, out=None):
+    """pss_prune on a wide root (any n < 2^63)."""
+    _need(root, True, "pss_prune_wide")
+    if out is not None:
+        cand, n_cand = out
+    else:
+        cand = torch.empty((root.k,), dtype=root.items.dtype, device=root.items.device)
+        n_cand = torch.empty((1,), dtype=torch.uint32, device=root.items.device)
+    c = root._c()
+    _check("pss_prune_wide", _lib.pss_prune_wide(ctypes.byref(c), n, cand.data_ptr(),
+                                                 n_cand.data_ptr(), _stream(stream)))
+    return cand, n_cand
 
 
 def pss_prune(root: Summaries, n: int, stream=None, out=None):
@@ -235,7 +310,7 @@ def pss_verify(A: torch.Tensor, cand: torch.Tensor, n_cand: torch.Tensor | None 
         raise TypeError("candidate and key types differ")
     cap = cand.numel()
     out = out if out is not None else torch.zeros((max(cap, 1),), dtype=torch.uint64, device=A.device)
-    ws = _ws(pss_workspace_bytes(OP_VERIFY, A.numel(), cap, 1, kt), workspace, A.device)
+    ws = _ws(pss_workspace_bytes(OP_VERIFY, A.numel(), cap, 1, kt), workspace, A.device, stream)
     _check("pss_verify", _lib.pss_verify(A.data_ptr(), A.numel(), kt, cand.data_ptr(), cap,
                                          n_cand.data_ptr() if n_cand is not None else None,
                                          out.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -267,7 +342,7 @@ def pss_query(A: torch.Tensor, k: int, P: int, workspace: torch.Tensor | None = 
     items = torch.empty((k,), dtype=_key_dtype(kt), device=A.device)
     counts = torch.empty((k,), dtype=torch.uint64, device=A.device)
     length = torch.zeros((1,), dtype=torch.uint32, device=A.device)
-    ws = _ws(pss_workspace_bytes(OP_QUERY, A.numel(), k, P, kt), workspace, A.device)
+    ws = _ws(pss_workspace_bytes(OP_QUERY, A.numel(), k, P, kt), workspace, A.device, stream)
     _check("pss_query", _lib.pss_query(A.data_ptr(), A.numel(), kt, k, P, items.data_ptr(),
                                        counts.data_ptr(), length.data_ptr(), ws.data_ptr(),
                                        ws.numel(), _stream(stream)))
@@ -283,8 +358,11 @@ def pss_query_host(A_host: torch.Tensor, k: int, P: int, d_A: torch.Tensor | Non
     kt = _key_type(A_host)
     n = A_host.numel()
     dev = torch.device("cuda", torch.cuda.current_device())
-    d_A = d_A if d_A is not None else torch.empty((max(n, 1),), dtype=A_host.dtype, device=dev)
-    ws = _ws(pss_workspace_bytes(OP_QUERY, n, k, P, kt), workspace, dev)
+    if d_A is None:
+        d_A = torch.empty((max(n, 1),), dtype=A_host.dtype, device=dev)
+        if stream is not None:
+            d_A.record_stream(stream)
+    ws = _ws(pss_workspace_bytes(OP_QUERY, n, k, P, kt), workspace, dev, stream)
     if out is None:
         pin = torch.cuda.is_available()
         out = (torch.empty((k,), dtype=_key_dtype(kt), pin_memory=pin),
@@ -407,7 +485,7 @@ def pss_exact_kmajority(A: torch.Tensor, k: int, workspace: torch.Tensor | None 
     counts = torch.empty((k,), dtype=torch.uint64, device=A.device)
     length = torch.zeros((1,), dtype=torch.uint32, device=A.device)
     overflow = torch.zeros((1,), dtype=torch.uint32, device=A.device)
-    ws = _ws(pss_workspace_bytes(OP_EXACT, A.numel(), k, 0, kt), workspace, A.device)
+    ws = _ws(pss_workspace_bytes(OP_EXACT, A.numel(), k, 0, kt), workspace, A.device, stream)
     _check("pss_exact_kmajority", _lib.pss_exact_kmajority(
         A.data_ptr(), A.numel(), kt, k, items.data_ptr(), counts.data_ptr(), length.data_ptr(),
         overflow.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -445,7 +523,7 @@ def pss_summarize_hybrid(A: torch.Tensor, k: int, Pp: int, T: int, out: Summarie
     A = _dev_keys(A)
     kt = _key_type(A)
     out = out or Summaries.empty(Pp * T, k, kt, A.device)
-    ws = _ws(pss_hybrid_workspace_bytes(A.numel(), k, Pp, T, kt), workspace, A.device)
+    ws = _ws(pss_hybrid_workspace_bytes(A.numel(), k, Pp, T, kt), workspace, A.device, stream)
     c = out._c()
     _check("pss_summarize_hybrid", _lib.pss_summarize_hybrid(
         A.data_ptr(), A.numel(), kt, k, Pp, T, ctypes.byref(c), ws.data_ptr(), ws.numel(),
@@ -458,7 +536,7 @@ def pss_merge_hybrid(leaves: Summaries, T: int, out: Summaries | None = None,
     """Per-process fixed trees over groups of T leaves, then the fixed tree over the roots."""
     out = out or Summaries.empty(1, leaves.k, leaves.key_type, leaves.items.device)
     ws = _ws(pss_hybrid_workspace_bytes(0, leaves.k, leaves.count // max(T, 1), T, leaves.key_type),
-             workspace, leaves.items.device)
+             workspace, leaves.items.device, stream)
     a, b = leaves._c(), out._c()
     _check("pss_merge_hybrid", _lib.pss_merge_hybrid(ctypes.byref(a), T, ctypes.byref(b),
                                                      ws.data_ptr(), ws.numel(), _stream(stream)))

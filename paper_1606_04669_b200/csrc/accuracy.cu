@@ -48,10 +48,15 @@ struct GSet {  // global open-addressing set: state 0 empty, 1 being written, 2 
   uint32_t* overflow;
 };
 
+// a linear probe longer than this means the set is (nearly) full: the result is reported
+// incomplete (overflow = 1) instead of scanning the whole table for every later key
+constexpr uint32_t GSET_MAX_PROBE = 1024;
+
 template <typename KT>
 __device__ void gset_insert(const GSet<KT>& g, KT x) {
+  if (__ldcg(g.overflow)) return;  // already incomplete
   uint32_t h = mix_hash(x) & g.mask;
-  for (uint32_t probe = 0; probe <= g.mask;) {
+  for (uint32_t probe = 0; probe <= min(g.mask, GSET_MAX_PROBE);) {
     const uint32_t s = ld_acquire(&g.state[h]);
     if (s == 0) {
       if (atomicCAS(&g.state[h], 0u, 1u) == 0u) {
@@ -73,7 +78,7 @@ __device__ void gset_insert(const GSet<KT>& g, KT x) {
 template <typename KT>
 __device__ __forceinline__ int64_t gset_find(const GSet<KT>& g, KT x) {
   uint32_t h = mix_hash(x) & g.mask;
-  for (uint32_t probe = 0; probe <= g.mask; ++probe) {
+  for (uint32_t probe = 0; probe <= min(g.mask, GSET_MAX_PROBE); ++probe) {
     if (g.state[h] == 0) return -1;
     if (g.keys[h] == x) return h;
     h = (h + 1) & g.mask;

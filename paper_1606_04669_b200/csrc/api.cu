@@ -117,6 +117,62 @@ const char* pss_status_string(pss_status s) {
   return "PSS_UNKNOWN_STATUS";
 }
 
+static bool wsummaries_ok(const pss_wsummaries* s) {
+  return s && key_bytes(s->key_type) && s->items && s->counts && s->errs && s->sizes &&
+         s->k >= 2 && s->count >= 1;
+}
+
+pss_status pss_widen(const pss_summaries* in, pss_wsummaries* out, cudaStream_t stream) {
+  if (!summaries_ok(in) || !wsummaries_ok(out)) return PSS_ERR_INVALID_ARG;
+  if (in->k != out->k || in->key_type != out->key_type || in->count != out->count)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  return cuda_status(widen_launch(key_bytes(in->key_type), in->k, in->count, in->items,
+                                  in->counts, in->errs, in->sizes, out->items, out->counts,
+                                  out->errs, out->sizes, stream));
+}
+
+pss_status pss_combine_wide(const pss_wsummaries* a, const pss_wsummaries* b,
+                            pss_wsummaries* out, void* d_ws, size_t ws_bytes,
+                            cudaStream_t stream) {
+  if (!wsummaries_ok(a) || !wsummaries_ok(b) || !wsummaries_ok(out) || !d_ws)
+    return PSS_ERR_INVALID_ARG;
+  if (a->k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (a->k != b->k || a->k != out->k || a->key_type != b->key_type ||
+      a->key_type != out->key_type || a->count != b->count || a->count != out->count)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const int kb = key_bytes(a->key_type);
+  const DevInfo d = dev_info();
+  if (ws_bytes < wide_combine_ws(kb, a->k, d) + 256) return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(wide_combine_launch(kb, a->k, a->count, a->items, a->counts, a->errs,
+                                         a->sizes, b->items, b->counts, b->errs, b->sizes,
+                                         out->items, out->counts, out->errs, out->sizes, d_ws,
+                                         stream, d));
+}
+
+pss_status pss_merge_wide(const pss_wsummaries* nodes, pss_wsummaries* root, void* d_ws,
+                          size_t ws_bytes, cudaStream_t stream) {
+  if (!wsummaries_ok(nodes) || !wsummaries_ok(root) || !d_ws) return PSS_ERR_INVALID_ARG;
+  if (nodes->k > PSS_MAX_K) return PSS_ERR_UNSUPPORTED;
+  if (root->k != nodes->k || root->key_type != nodes->key_type || root->count != 1)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const int kb = key_bytes(nodes->key_type);
+  const DevInfo d = dev_info();
+  if (ws_bytes < wide_merge_ws(kb, nodes->k, nodes->count, d) + 256)
+    return PSS_ERR_WORKSPACE_TOO_SMALL;
+  return cuda_status(wide_merge_launch(kb, nodes->k, nodes->count, nodes->items, nodes->counts,
+                                       nodes->errs, nodes->sizes, root->items, root->counts,
+                                       root->errs, root->sizes, d_ws, stream, d));
+}
+
+pss_status pss_prune_wide(const pss_wsummaries* root, uint64_t n, void* d_cand,
+                          uint32_t* d_n_cand, cudaStream_t stream) {
+  if (!wsummaries_ok(root) || !d_cand || !d_n_cand || root->count != 1)
+    return PSS_ERR_INVALID_ARG;
+  if (n >> 63) return PSS_ERR_UNSUPPORTED;
+  return cuda_status(wide_prune_launch(key_bytes(root->key_type), root->items, root->counts,
+                                       root->sizes, n, root->k, d_cand, d_n_cand, stream));
+}
+
 const char* pss_version(void) { return "pss-b200 0.1 (sm_100a)"; }
 
 size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_type kt) {
@@ -131,6 +187,8 @@ size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_t
     case PSS_OP_QUERY: return q_layout(n, kb, k, P ? P : 1, d).total;
     case PSS_OP_EXACT: return exact_ws(kb, n, k);
     case PSS_OP_SUMMARIZE_MERGE: return sm_layout(n, kb, k, P ? P : 1, d).total;
+    case PSS_OP_COMBINE_WIDE: return wide_combine_ws(kb, k, d) + 256;
+    case PSS_OP_MERGE_WIDE: return wide_merge_ws(kb, k, P ? P : 1, d) + 256;
   }
   return 0;
 }
@@ -202,7 +260,7 @@ pss_status pss_combine(const pss_summaries* a, const pss_summaries* b, pss_summa
 pss_status pss_prune(const pss_summaries* root, uint64_t n, void* d_cand, uint32_t* d_n_cand,
                      cudaStream_t stream) {
   if (!summaries_ok(root) || !d_cand || !d_n_cand || root->count != 1) return PSS_ERR_INVALID_ARG;
-  if (n > PSS_MAX_N) return PSS_ERR_UNSUPPORTED;
+  if (n >> 63) return PSS_ERR_UNSUPPORTED;  // the threshold is 64-bit arithmetic
   return cuda_status(prune_launch(key_bytes(root->key_type), root->k, root->items, root->counts,
                                   root->sizes, n, d_cand, d_n_cand, stream));
 }
@@ -225,7 +283,7 @@ pss_status pss_report(const void* d_cand, uint32_t n_cand, const uint32_t* d_n_c
   const int kb = key_bytes(kt);
   if (!kb || k < 2 || !d_out_len || (n_cand && (!d_cand || !d_exact || !d_out_items || !d_out_counts)))
     return PSS_ERR_INVALID_ARG;
-  if (n > PSS_MAX_N) return PSS_ERR_UNSUPPORTED;
+  if (n >> 63) return PSS_ERR_UNSUPPORTED;  // 64-bit threshold and exact counts
   return cuda_status(result_launch(kb, n_cand, d_cand, d_n_cand, d_exact, n, k, d_out_items,
                                    d_out_counts, d_out_len, stream));
 }

@@ -167,6 +167,24 @@ cudaError_t hist_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t 
                         uint32_t* counts, uint32_t* errs, uint32_t* sizes, uint32_t* queue,
                         unsigned char* flagged, cudaStream_t s, const DevInfo& d, uint32_t r0,
                         uint32_t r1, uint32_t T, uint32_t* leaf_flags);
+// wide.cu: summaries with 64-bit counts and errors (the tree above the leaves, > 2^31 items)
+size_t wide_combine_ws(int kb, uint32_t k, const DevInfo& d);
+size_t wide_merge_ws(int kb, uint32_t k, uint32_t count, const DevInfo& d);
+cudaError_t wide_combine_launch(int kb, uint32_t k, uint32_t count, const void* ai,
+                                const uint64_t* ac, const uint64_t* ae, const uint32_t* as,
+                                const void* bi, const uint64_t* bc, const uint64_t* be,
+                                const uint32_t* bs, void* oi, uint64_t* oc, uint64_t* oe,
+                                uint32_t* os, void* scratch, cudaStream_t s, const DevInfo& d);
+cudaError_t wide_merge_launch(int kb, uint32_t k, uint32_t count, const void* items,
+                              const uint64_t* counts, const uint64_t* errs, const uint32_t* sizes,
+                              void* ri, uint64_t* rc, uint64_t* re, uint32_t* rs, void* ws,
+                              cudaStream_t s, const DevInfo& d);
+cudaError_t widen_launch(int kb, uint32_t k, uint32_t count, const void* items,
+                         const uint32_t* counts, const uint32_t* errs, const uint32_t* sizes,
+                         void* wi, uint64_t* wc, uint64_t* we, uint32_t* wsz, cudaStream_t s);
+cudaError_t wide_prune_launch(int kb, const void* items, const uint64_t* counts,
+                              const uint32_t* sizes, uint64_t n, uint32_t k, void* cand,
+                              uint32_t* n_cand, cudaStream_t s);
 // partition queues in the summarize workspace: launches over disjoint ranges [r0, r1) that may be
 // in flight together use distinct qi < SS_MAX_RANGES
 constexpr uint32_t SS_MAX_RANGES = 64;

@@ -11,7 +11,7 @@
 // over the block's positions. As soon as the block shows more than min(k, 3/4 of the table)
 // distinct keys the CTA gives up on it and flags it; K1 (summarize.cu) then runs the sequential
 // rule on the flagged blocks only. Both produce the same leaf bit for bit (the GPU parity tests
-// compare every leaf with the oracle's sequential Space Saving).
+// compare every leaf with sequential Space Saving run on the CPU).
 #include <cstdlib>
 
 #include "common.cuh"

@@ -793,29 +793,6 @@ static cudaError_t combine_run(int kb, uint32_t k, CombArgs a, void* ws, cudaStr
   fill_comb_args(a, kb, k, p, ws);
   if (a.nblocks == 0) return cudaSuccess;
   const int grid = (int)std::min<uint32_t>(a.nblocks, (uint32_t)p.grid_cap);
-  // Internal nodes (select, no sort): wide levels are throughput-bound and
-  // take small CTAs (more COMBINEs resident per SM), narrow levels are latency-bound and take
-  // the largest CTAs (fewer counters per thread).
-  if (!a.sort_out && !p.g && k >= 256) {
-    const char* lvh = std::getenv("PSS_DEBUG_MERGE_LEVEL_NT");  // experiment hook: "wide,narrow"
-    int wide_nt = 512, narrow_nt = 1024;
-    if (lvh) sscanf(lvh, "%d,%d", &wide_nt, &narrow_nt);
-    const int nt = a.nblocks >= 2u * (uint32_t)d.sms ? wide_nt : narrow_nt;
-    const size_t sm = p.smem;  // the exchange buffer holds the tie list
-    auto go = [&](auto kt) {
-      using KT = decltype(kt);
-      switch (nt) {
-        case 256: launch_comb<KT, false, 256, 0>(a, grid, sm, s); break;
-        case 1024: launch_comb<KT, false, 1024, 0>(a, grid, sm, s); break;
-        default: launch_comb<KT, false, 512, 0>(a, grid, sm, s); break;
-      }
-    };
-    if (kb == 4)
-      go(uint32_t{});
-    else
-      go(uint64_t{});
-    return cudaGetLastError();
-  }
   bool ok;
   if (kb == 4)
     ok = p.g ? dispatch_comb<uint32_t, true>(a, grid, p, s) : dispatch_comb<uint32_t, false>(a, grid, p, s);

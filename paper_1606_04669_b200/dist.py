@@ -10,8 +10,11 @@ exactly the rank-local blocks (floor(r*n/P) offsets), and with world and P power
 form one complete subtree of the fixed binary tree (R6). Each rank reduces its subtree to a root;
 ONE all-gather moves the world roots (k counters each) over NVLink, and every rank finishes the
 top log2(world) levels of the same tree in the same order, so the global root is bit-identical to
-the single-GPU one. Verification counts the local shard and ONE all-reduce(sum) adds the exact
-counts. The collectives are torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+the single-GPU one. Those top levels run on wide summaries (64-bit counts, pss_merge_wide): each
+rank's shard holds at most 2^31 keys, but world shards together may exceed 2^31 (weak scaling of
+the 2^29-key workload to 8 GPUs is 2^32 keys), beyond reading R9's u32 bound. Verification counts
+the local shard and ONE all-reduce(sum) adds the exact (uint64) counts. The collectives are
+torch.distributed (NCCL on GPUs, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -19,9 +22,9 @@ import math
 
 import torch
 
-from . import (KEY_U32, OP_MERGE, OP_SUMMARIZE_MERGE, OP_VERIFY, Summaries, _key_dtype,
-               pss_merge, pss_prune, pss_query_host, pss_report, pss_summarize_merge, pss_verify,
-               pss_workspace_bytes)
+from . import (KEY_U32, OP_MERGE_WIDE, OP_SUMMARIZE_MERGE, OP_VERIFY, Summaries, _key_dtype,
+               pss_merge_wide, pss_prune, pss_prune_wide, pss_query_host, pss_report,
+               pss_summarize_merge, pss_verify, pss_widen, pss_workspace_bytes)
 
 
 def shard(n_total: int, world: int, rank: int) -> tuple[int, int]:
@@ -102,11 +105,17 @@ class Runner:
         self.world, self.rank, self.group = world, rank, group
         self.dev = torch.device(device)
         kb = 4 if key_type == KEY_U32 else 8
+        if n > (1 << 31):
+            raise ValueError("a rank's shard holds at most 2^31 keys (u32 leaf counters, R9)")
         self.leaves = Summaries.empty(P, k, key_type, self.dev)
         self.root = Summaries.empty(1, k, key_type, self.dev)
-        self.top = Summaries.empty(1, k, key_type, self.dev) if world > 1 else self.root
+        if world > 1:  # the top levels over the ranks' roots: 64-bit counts (wide summaries)
+            self.gathered_w = Summaries.empty(world, k, key_type, self.dev, wide=True)
+            self.top = Summaries.empty(1, k, key_type, self.dev, wide=True)
+        else:
+            self.top = self.root
         ws = max(pss_workspace_bytes(OP_SUMMARIZE_MERGE, n, k, P, key_type),
-                 pss_workspace_bytes(OP_MERGE, 0, k, max(P, world), key_type),
+                 pss_workspace_bytes(OP_MERGE_WIDE, 0, k, world, key_type),
                  pss_workspace_bytes(OP_VERIFY, n, k, 1, key_type))
         self.ws = torch.empty((ws,), dtype=torch.uint8, device=self.dev)
         self.exact = torch.zeros((k,), dtype=torch.uint64, device=self.dev)
@@ -117,8 +126,11 @@ class Runner:
                     torch.empty((k,), dtype=torch.uint64, device=self.dev),
                     torch.zeros((1,), dtype=torch.uint32, device=self.dev))
         self.host_out = tuple(torch.empty_like(t, device="cpu").pin_memory() for t in self.out)
+        # K1 (+ the histogram kernel when used), the tree, [widen + one wide COMBINE launch per
+        # top level], prune, verify (setup, scan, finalize), report
+        top_levels = (world - 1).bit_length() if world > 1 else 0
         self.launches_per_step = (1 + _merge_launches(P, k, kb) +
-                                  (_merge_launches(world, k, kb) if world > 1 else 0) + 1 + 3 + 1)
+                                  (1 + top_levels if world > 1 else 0) + 1 + 3 + 1)
         self.host_api = "pss_query_host" if world == 1 else "H2D copy + step + D2H (torch)"
         self._kb = kb
 
@@ -134,10 +146,14 @@ class Runner:
         n_global = self.n * self.world
         if self.world > 1:
             gathered = gather_summaries(self.root, self.group)
-            pss_merge(gathered, out=self.top, workspace=self.ws)
+            pss_widen(gathered, out=self.gathered_w)
+            pss_merge_wide(self.gathered_w, out=self.top, workspace=self.ws)
         if ev is not None:
             ev[2].record(s)
-        cand, n_cand = pss_prune(self.top, n_global, out=self.cand)
+        if self.world > 1:
+            cand, n_cand = pss_prune_wide(self.top, n_global, out=self.cand)
+        else:
+            cand, n_cand = pss_prune(self.top, n_global, out=self.cand)
         exact = pss_verify(A, cand, n_cand, out=self.exact, workspace=self.ws)
         if self.world > 1:
             allreduce_counts(self.exact, self.group)

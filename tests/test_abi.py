@@ -201,3 +201,25 @@ def test_read_probe_validation(pss):
     assert lib.pss_read_probe(ctypes.c_void_p(0x1004), 10, 0, ctypes.c_void_p(0x1000), None) == 1
     assert lib.pss_read_probe(ctypes.c_void_p(0x1000), 10, 0, None, None) == 1
     assert lib.pss_read_probe(ctypes.c_void_p(0x1000), 10, 9, ctypes.c_void_p(0x1000), None) == 1
+
+
+def test_wide_validation_before_launch(pss):
+    """The wide-summary calls (64-bit counts) validate like their narrow twins."""
+    lib = pss._lib
+    S = pss._Summ
+    dummy = ctypes.c_void_p(0x1000)
+    by = ctypes.byref
+    a = S(0, 10, 4, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_widen(None, by(a), None) == 1
+    assert lib.pss_widen(by(a), by(S(0, 11, 4, 0x1000, 0x1000, 0x1000, 0x1000)), None) == 3
+    assert lib.pss_combine_wide(by(a), by(S(1, 10, 4, 0x1000, 0x1000, 0x1000, 0x1000)), by(a),
+                                dummy, 1 << 30, None) == 3
+    assert lib.pss_combine_wide(by(a), by(a), by(a), None, 1 << 30, None) == 1
+    assert lib.pss_merge_wide(by(a), by(S(0, 10, 2, 0x1000, 0x1000, 0x1000, 0x1000)), dummy,
+                              1 << 30, None) == 3
+    assert lib.pss_merge_wide(by(a), by(S(0, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)), dummy,
+                              16, None) == 4
+    root = S(0, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_prune_wide(by(a), 100, dummy, dummy, None) == 1  # count != 1
+    assert lib.pss_prune_wide(by(root), 1 << 63, dummy, dummy, None) == 2
+    assert lib.pss_prune_wide(by(root), 100, None, dummy, None) == 1

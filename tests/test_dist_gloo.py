@@ -64,7 +64,7 @@ def _worker(rank, world, port, n_total, k, P_per, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,P_per", [(2, 4), (4, 2)])
+@pytest.mark.parametrize("world,P_per", [(2, 4), (4, 2), (8, 1), (8, 2)])
 def test_sharded_tree_is_bit_identical(world, P_per):
     from conftest import build_lib
     build_lib()

@@ -35,7 +35,8 @@ def _worker(rank, world, port, n_local, k, P, q):
         items, counts, ln = r.step(torch.from_numpy(A).cuda())
         torch.cuda.synchronize()
         m = int(ln.item())
-        q.put((rank, items[:m].cpu().numpy().tolist(), counts[:m].cpu().numpy().tolist()))
+        q.put((rank, items[:m].cpu().numpy().tolist(), counts[:m].cpu().numpy().tolist(),
+               r.top.host(0)))
     finally:
         dist.destroy_process_group()
 
@@ -74,3 +75,6 @@ def test_two_ranks_match_one(pss_lib=None):
     assert res[0][2] == counts[:m].cpu().numpy().tolist()
     ref = oracle.pipeline(A, k, world * P, threads=8)
     assert res[0][1] == ref.result[0].tolist() and res[0][2] == ref.result[1].tolist()
+    # the gathered top of the tree (wide summaries) on every rank is the oracle's root
+    for r in res:
+        assert r[3] == ref.root.as_tuples()
