@@ -246,8 +246,10 @@ pss_status pss_query_host(const void* h_A, void* d_A, uint64_t n, pss_key_type k
  * State: a pss_stream (host struct, caller-owned; written by pss_stream_init and every feed) plus
  * a device workspace of pss_stream_workspace_bytes(...) bytes that holds the subtree stack, the
  * partial leaf, a batch of leaf summaries and the host-feed buffers. A stream is used by one host
- * thread and one CUDA stream at a time. Stream length: N + floor(N/k) <= 2^32 - 1 (u32 counters,
- * R9), i.e. N <= floor((2^32 - 1) k / (k + 1)); a feed past it returns PSS_ERR_UNSUPPORTED and
+ * thread and one CUDA stream at a time. Counts: a leaf and a block of batch_leaves leaves hold at
+ * most 2^31 items (u32 counters, R9); the subtree stack and the fold above the blocks keep 64-bit
+ * counts (pss_wsummaries), so a stream may reach N = 2^63 items (P:195's streams of 29 10^9 items,
+ * beyond one GPU's HBM when fed from the host); a feed past it returns PSS_ERR_UNSUPPORTED and
  * changes nothing.
  */
 typedef struct {
@@ -283,7 +285,12 @@ pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t le
                                 cudaStream_t stream);
 
 /* The summary of the stream so far (the R6 tree over its leaves, the partial leaf included), in
- * canonical order (R5) into root (count 1, same k and key type). Does not change the stream. */
+ * canonical order (R5) into root (count 1, same k and key type), with 64-bit counts. Does not
+ * change the stream. */
+pss_status pss_stream_root_wide(const pss_stream* st, pss_wsummaries* root, cudaStream_t stream);
+
+/* The same root with u32 counts: only while N + floor(N/k) < 2^32 (N <= floor((2^32 - 1) k /
+ * (k + 1)), R9), else PSS_ERR_UNSUPPORTED. */
 pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream_t stream);
 
 /*

@@ -393,10 +393,12 @@ _lib.pss_stream_init.argtypes = [_STP, _i32, _u32, _u32, _u32, _vp, _sz]
 _lib.pss_stream_feed.argtypes = [_STP, _vp, _u64, _vp]
 _lib.pss_stream_feed_host.argtypes = [_STP, _vp, _u64, _vp]
 _lib.pss_stream_root.argtypes = [_STP, _SP, _vp]
-for _f in ("pss_stream_init", "pss_stream_feed", "pss_stream_feed_host", "pss_stream_root"):
+_lib.pss_stream_root_wide.argtypes = [_STP, _SP, _vp]
+for _f in ("pss_stream_init", "pss_stream_feed", "pss_stream_feed_host", "pss_stream_root",
+           "pss_stream_root_wide"):
     getattr(_lib, _f).restype = _i32
 EXPORTED_SYMBOLS += ["pss_stream_workspace_bytes", "pss_stream_init", "pss_stream_feed",
-                     "pss_stream_feed_host", "pss_stream_root"]
+                     "pss_stream_feed_host", "pss_stream_root", "pss_stream_root_wide"]
 __all__ += ["Stream", "pss_stream_workspace_bytes"]
 
 
@@ -444,12 +446,13 @@ class Stream:
                                      chunk.numel(), _stream(stream)))
         return self
 
-    def root(self, out: Summaries | None = None, stream=None) -> Summaries:
-        """The summary of the stream so far, canonical order (one summary)."""
-        out = out or Summaries.empty(1, self.k, self.key_type, self.ws.device)
+    def root(self, out: Summaries | None = None, stream=None, wide: bool = False) -> Summaries:
+        """The summary of the stream so far, canonical order (one summary); wide = 64-bit
+        counts (required once n_seen + n_seen / k reaches 2^32)."""
+        out = out or Summaries.empty(1, self.k, self.key_type, self.ws.device, wide=wide)
         c = out._c()
-        _check("pss_stream_root", _lib.pss_stream_root(ctypes.byref(self._st), ctypes.byref(c),
-                                                       _stream(stream)))
+        fn = _lib.pss_stream_root_wide if out.wide else _lib.pss_stream_root
+        _check("pss_stream_root", fn(ctypes.byref(self._st), ctypes.byref(c), _stream(stream)))
         return out
 
 

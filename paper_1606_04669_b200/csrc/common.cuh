@@ -182,6 +182,9 @@ cudaError_t wide_merge_launch(int kb, uint32_t k, uint32_t count, const void* it
 cudaError_t widen_launch(int kb, uint32_t k, uint32_t count, const void* items,
                          const uint32_t* counts, const uint32_t* errs, const uint32_t* sizes,
                          void* wi, uint64_t* wc, uint64_t* we, uint32_t* wsz, cudaStream_t s);
+cudaError_t narrow_launch(int kb, uint32_t k, uint32_t count, const void* wi, const uint64_t* wc,
+                          const uint64_t* we, const uint32_t* wsz, void* items, uint32_t* counts,
+                          uint32_t* errs, uint32_t* sizes, cudaStream_t s);
 cudaError_t wide_prune_launch(int kb, const void* items, const uint64_t* counts,
                               const uint32_t* sizes, uint64_t n, uint32_t k, void* cand,
                               uint32_t* n_cand, cudaStream_t s);

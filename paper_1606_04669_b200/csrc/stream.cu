@@ -15,7 +15,11 @@
 // down, then the summary of the partial leaf: this is the R6 tree over all the leaves (R6's root
 // splits off its largest complete left subtree, recursively).
 //
-// Host code only: the kernels are K1 (summarize.cu) and K2 (merge.cu).
+// Counts: a block holds at most batch_leaves * leaf_len <= 2^31 items, so leaves and block roots
+// keep u32 counts (R9); the stack and the fold above the blocks use 64-bit counts (wide.cu), so a
+// stream may reach 2^63 items -- beyond one GPU's HBM when fed from the host (P:195's 29 10^9).
+//
+// Host code only: the kernels are K1 (summarize.cu, hist.cu), K2 (merge.cu) and wide.cu.
 #include <algorithm>
 
 #include "common.cuh"
@@ -25,13 +29,14 @@ namespace pss {
 namespace {
 
 struct StreamLayout {
-  size_t stk_items, stk_counts, stk_errs, stk_sizes;  // STACK_LEVELS summaries
-  size_t tmp_items, tmp_counts, tmp_errs, tmp_sizes;  // 3 summaries: block root, carry ping-pong
+  size_t stk_items, stk_counts, stk_errs, stk_sizes;  // STACK_LEVELS wide summaries
+  size_t wt_items, wt_counts, wt_errs, wt_sizes;      // 4 wide: block root, fold ping-pong, leaf
+  size_t nt_items, nt_counts, nt_errs, nt_sizes;      // 1 narrow: a block's root from the tree
   size_t b_items, b_counts, b_errs, b_sizes;          // batch_leaves leaf summaries
   size_t staging;                                     // leaf_len keys: the partial leaf
   size_t hostbuf;                                     // 2 x batch_leaves * leaf_len keys (feed_host)
   size_t flags;                                       // batch_leaves ready flags (K1 -> tree)
-  size_t sumscratch, scratch, total;                  // K1's and the tree's (they overlap)
+  size_t sumscratch, scratch, wscratch, total;        // K1's, the tree's, the wide COMBINE's
 };
 constexpr uint32_t STACK_LEVELS = 64;
 
@@ -40,13 +45,17 @@ StreamLayout stream_layout(int kb, uint32_t k, uint32_t leaf_len, uint32_t batch
   StreamLayout L;
   Bump b;
   L.stk_items = b.take<unsigned char>((size_t)STACK_LEVELS * k * kb);
-  L.stk_counts = b.take<uint32_t>((size_t)STACK_LEVELS * k);
-  L.stk_errs = b.take<uint32_t>((size_t)STACK_LEVELS * k);
+  L.stk_counts = b.take<uint64_t>((size_t)STACK_LEVELS * k);
+  L.stk_errs = b.take<uint64_t>((size_t)STACK_LEVELS * k);
   L.stk_sizes = b.take<uint32_t>(STACK_LEVELS);
-  L.tmp_items = b.take<unsigned char>((size_t)3 * k * kb);
-  L.tmp_counts = b.take<uint32_t>((size_t)3 * k);
-  L.tmp_errs = b.take<uint32_t>((size_t)3 * k);
-  L.tmp_sizes = b.take<uint32_t>(3);
+  L.wt_items = b.take<unsigned char>((size_t)4 * k * kb);
+  L.wt_counts = b.take<uint64_t>((size_t)4 * k);
+  L.wt_errs = b.take<uint64_t>((size_t)4 * k);
+  L.wt_sizes = b.take<uint32_t>(4);
+  L.nt_items = b.take<unsigned char>((size_t)k * kb);
+  L.nt_counts = b.take<uint32_t>(k);
+  L.nt_errs = b.take<uint32_t>(k);
+  L.nt_sizes = b.take<uint32_t>(1);
   L.b_items = b.take<unsigned char>((size_t)batch * k * kb);
   L.b_counts = b.take<uint32_t>((size_t)batch * k);
   L.b_errs = b.take<uint32_t>((size_t)batch * k);
@@ -57,16 +66,24 @@ StreamLayout stream_layout(int kb, uint32_t k, uint32_t leaf_len, uint32_t batch
   const uint64_t nb = (uint64_t)batch * leaf_len;
   L.sumscratch = b.take<unsigned char>(
       std::max(summarize_ws(nb, kb, k, batch, d), summarize_ws(leaf_len, kb, k, 1, d)));
-  L.scratch = b.take<unsigned char>(std::max(merge_ws(kb, k, batch, d), combine_ws(kb, k, 1, d)));
+  L.scratch = b.take<unsigned char>(merge_ws(kb, k, batch, d));
+  L.wscratch = b.take<unsigned char>(
+      std::max(wide_combine_ws(kb, k, d), wide_merge_ws(kb, k, 1, d)));
   L.total = b.bytes();
   return L;
 }
 
-// a view of one summary inside a workspace region of `cap` summaries
+// a view of one summary inside a workspace region (narrow: u32 counts, wide: u64 counts)
 struct One {
   void* items;
   uint32_t* counts;
   uint32_t* errs;
+  uint32_t* sizes;
+};
+struct WOne {
+  void* items;
+  uint64_t* counts;
+  uint64_t* errs;
   uint32_t* sizes;
 };
 
@@ -82,22 +99,41 @@ struct StreamCtx {
                reinterpret_cast<uint32_t*>(w + oe) + (size_t)i * k,
                reinterpret_cast<uint32_t*>(w + os) + i};
   }
-  One stack(uint32_t j) const { return region(L.stk_items, L.stk_counts, L.stk_errs, L.stk_sizes, j); }
-  One tmp(uint32_t i) const { return region(L.tmp_items, L.tmp_counts, L.tmp_errs, L.tmp_sizes, i); }
+  WOne wregion(size_t oi, size_t oc, size_t oe, size_t os, uint32_t i) const {
+    return WOne{w + oi + (size_t)i * k * kb, reinterpret_cast<uint64_t*>(w + oc) + (size_t)i * k,
+                reinterpret_cast<uint64_t*>(w + oe) + (size_t)i * k,
+                reinterpret_cast<uint32_t*>(w + os) + i};
+  }
+  WOne stack(uint32_t j) const {
+    return wregion(L.stk_items, L.stk_counts, L.stk_errs, L.stk_sizes, j);
+  }
+  WOne wtmp(uint32_t i) const { return wregion(L.wt_items, L.wt_counts, L.wt_errs, L.wt_sizes, i); }
+  One ntmp() const { return region(L.nt_items, L.nt_counts, L.nt_errs, L.nt_sizes, 0); }
   One leaf(uint32_t i) const { return region(L.b_items, L.b_counts, L.b_errs, L.b_sizes, i); }
   void* scratch() const { return w + L.scratch; }
 
-  // the R6 root of `cnt` consecutive summaries starting at `first` (cnt = 1: canonical copy);
-  // with leaf_flags, a tree kernel overlapping the K1 launch that produces the leaves
+  // the R6 root of `cnt` consecutive leaf summaries starting at `first` (narrow: a block holds at
+  // most batch_leaves * leaf_len <= 2^31 items); with leaf_flags, a tree kernel overlapping the
+  // K1 launch that produces the leaves
   cudaError_t tree(const One& first, uint32_t cnt, const One& out, cudaStream_t s,
                    const uint32_t* leaf_flags = nullptr) const {
     return merge_tree_launch(kb, k, cnt, first.items, first.counts, first.errs, first.sizes,
                              out.items, out.counts, out.errs, out.sizes, scratch(), s, d,
                              leaf_flags);
   }
-  cudaError_t combine(const One& a, const One& b, const One& out, cudaStream_t s) const {
-    return combine_launch(kb, k, 1, a.items, a.counts, a.errs, a.sizes, b.items, b.counts, b.errs,
-                          b.sizes, out.items, out.counts, out.errs, out.sizes, scratch(), s, d);
+  cudaError_t widen(const One& in, const WOne& out, cudaStream_t s) const {
+    return widen_launch(kb, k, 1, in.items, in.counts, in.errs, in.sizes, out.items, out.counts,
+                        out.errs, out.sizes, s);
+  }
+  // above the blocks the stream may exceed 2^31 items: COMBINE with 64-bit counts (wide.cu)
+  cudaError_t combine(const WOne& a, const WOne& b, const WOne& out, cudaStream_t s) const {
+    return wide_combine_launch(kb, k, 1, a.items, a.counts, a.errs, a.sizes, b.items, b.counts,
+                               b.errs, b.sizes, out.items, out.counts, out.errs, out.sizes,
+                               w + L.wscratch, s, d);
+  }
+  cudaError_t canonical(const WOne& in, const WOne& out, cudaStream_t s) const {
+    return wide_merge_launch(kb, k, 1, in.items, in.counts, in.errs, in.sizes, out.items,
+                             out.counts, out.errs, out.sizes, w + L.wscratch, s, d);
   }
   cudaError_t summarize(const void* A, uint64_t n, uint32_t P, const One& out, cudaStream_t s,
                         uint32_t* leaf_flags = nullptr) const {
@@ -113,12 +149,14 @@ struct StreamCtx {
     uint32_t top = j;  // carries run while the sibling (bit `top` of p) is on the stack
     while (top < STACK_LEVELS && ((p >> top) & 1u)) ++top;
     if (top >= STACK_LEVELS) return cudaErrorInvalidValue;
-    if (top == j) return tree(first, 1u << j, stack(j), s, leaf_flags);
-    cudaError_t e = tree(first, 1u << j, tmp(0), s, leaf_flags);
+    cudaError_t e = tree(first, 1u << j, ntmp(), s, leaf_flags);
+    if (e != cudaSuccess) return e;
+    if (top == j) return widen(ntmp(), stack(j), s);
+    e = widen(ntmp(), wtmp(0), s);
     uint32_t cur = 0;
     for (uint32_t t = j; t < top && e == cudaSuccess; ++t) {
-      const One out = (t + 1 == top) ? stack(top) : tmp(cur == 1 ? 2 : 1);
-      e = combine(stack(t), tmp(cur), out, s);
+      const WOne out = (t + 1 == top) ? stack(top) : wtmp(cur == 1 ? 2 : 1);
+      e = combine(stack(t), wtmp(cur), out, s);
       cur = cur == 1 ? 2 : 1;
     }
     return e;
@@ -153,6 +191,35 @@ struct StreamCtx {
     }
     return e;
   }
+
+  // the summary of the stream so far (R6 tree over its leaves) into the wide summary `out`
+  cudaError_t root(uint64_t n_seen, const WOne& out, cudaStream_t s) const {
+    const uint64_t complete = n_seen / leaf_len, have = n_seen % leaf_len;
+    // the fold's operands from the right: the partial leaf, then stack levels upwards
+    WOne ops[STACK_LEVELS + 1];
+    uint32_t nops = 0;
+    cudaError_t e = cudaSuccess;
+    if (have) {
+      e = summarize(w + L.staging, have, 1, leaf(0), s);
+      if (e == cudaSuccess) e = widen(leaf(0), wtmp(3), s);
+      ops[nops++] = wtmp(3);
+    }
+    for (uint32_t j = 0; j < STACK_LEVELS; ++j)
+      if ((complete >> j) & 1u) ops[nops++] = stack(j);
+    if (e != cudaSuccess) return e;
+    if (nops == 0) return cudaMemsetAsync(out.sizes, 0, sizeof(uint32_t), s);
+    if (nops == 1) return canonical(ops[0], out, s);
+    // acc = ops[0]; acc = COMBINE(ops[i], acc) for i = 1..nops-1, the last one into `out`
+    WOne acc = ops[0];
+    uint32_t cur = 1;
+    for (uint32_t i = 1; i < nops && e == cudaSuccess; ++i) {
+      const WOne dst = (i + 1 == nops) ? out : wtmp(cur);
+      e = combine(ops[i], acc, dst, s);
+      acc = dst;
+      cur = cur == 1 ? 2 : 1;
+    }
+    return e;
+  }
 };
 
 bool ctx_of(const pss_stream* st, StreamCtx& c) {
@@ -169,11 +236,13 @@ bool ctx_of(const pss_stream* st, StreamCtx& c) {
   return st->ws_bytes >= c.L.total;
 }
 
-// f_hat <= N + floor(N/k) must fit the u32 counters (R9, invariant I of SURVEY.md 8(c))
-uint64_t stream_max_n(uint32_t k) {
+// a narrow (u32) root needs f_hat <= N + floor(N/k) <= 2^32 - 1 (R9, invariant I of SURVEY.md
+// 8(c)); the stream itself keeps 64-bit counts above its blocks and may grow to 2^63 items
+uint64_t stream_narrow_max_n(uint32_t k) {
   const uint64_t lim = 0xffffffffull;
   return lim * k / (k + 1);
 }
+constexpr uint64_t STREAM_MAX_N = 1ull << 63;
 
 // ingest len keys at d_chunk (device) into the stream described by c and st->n_seen
 cudaError_t feed_device(const StreamCtx& c, pss_stream* st, const void* d_chunk, uint64_t len,
@@ -250,7 +319,7 @@ pss_status pss_stream_feed(pss_stream* st, const void* d_chunk, uint64_t len,
   if (!st || (len && !d_chunk)) return PSS_ERR_INVALID_ARG;
   StreamCtx c;
   if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
-  if (st->n_seen + len > stream_max_n(st->k) || st->n_seen + len < st->n_seen)
+  if (st->n_seen + len > STREAM_MAX_N || st->n_seen + len < st->n_seen)
     return PSS_ERR_UNSUPPORTED;
   return feed_device(c, st, d_chunk, len, stream) == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
 }
@@ -260,7 +329,7 @@ pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t le
   if (!st || (len && !h_chunk)) return PSS_ERR_INVALID_ARG;
   StreamCtx c;
   if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
-  if (st->n_seen + len > stream_max_n(st->k) || st->n_seen + len < st->n_seen)
+  if (st->n_seen + len > STREAM_MAX_N || st->n_seen + len < st->n_seen)
     return PSS_ERR_UNSUPPORTED;
   if (!len) return PSS_OK;
   // pieces of one batch of leaves, copied on a private stream into two alternating device
@@ -299,6 +368,18 @@ pss_status pss_stream_feed_host(pss_stream* st, const void* h_chunk, uint64_t le
   return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
 }
 
+pss_status pss_stream_root_wide(const pss_stream* st, pss_wsummaries* root,
+                                cudaStream_t stream) {
+  if (!st || !root || !root->items || !root->counts || !root->errs || !root->sizes)
+    return PSS_ERR_INVALID_ARG;
+  StreamCtx c;
+  if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
+  if (root->k != st->k || root->key_type != st->key_type || root->count != 1)
+    return PSS_ERR_CAPACITY_MISMATCH;
+  const WOne out{root->items, root->counts, root->errs, root->sizes};
+  return c.root(st->n_seen, out, stream) == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
+}
+
 pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream_t stream) {
   if (!st || !root || !root->items || !root->counts || !root->errs || !root->sizes)
     return PSS_ERR_INVALID_ARG;
@@ -306,32 +387,13 @@ pss_status pss_stream_root(const pss_stream* st, pss_summaries* root, cudaStream
   if (!ctx_of(st, c)) return PSS_ERR_INVALID_ARG;
   if (root->k != st->k || root->key_type != st->key_type || root->count != 1)
     return PSS_ERR_CAPACITY_MISMATCH;
-  const One out{root->items, root->counts, root->errs, root->sizes};
-  const uint64_t complete = st->n_seen / st->leaf_len, have = st->n_seen % st->leaf_len;
-  // the fold's operands from the right: the partial leaf, then stack levels upwards
-  One ops[STACK_LEVELS + 1];
-  uint32_t nops = 0;
-  cudaError_t e = cudaSuccess;
-  if (have) {
-    ops[nops++] = c.leaf(0);
-    e = c.summarize(c.w + c.L.staging, have, 1, c.leaf(0), stream);
-  }
-  for (uint32_t j = 0; j < 64; ++j)
-    if ((complete >> j) & 1u) ops[nops++] = c.stack(j);
-  if (e != cudaSuccess) return PSS_ERR_CUDA;
-  if (nops == 0) return cudaMemsetAsync(root->sizes, 0, sizeof(uint32_t), stream) == cudaSuccess
-                            ? PSS_OK
-                            : PSS_ERR_CUDA;
-  if (nops == 1) return c.tree(ops[0], 1, out, stream) == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
-  // acc = ops[0]; acc = COMBINE(ops[i], acc) for i = 1..nops-1, the last one into `root`
-  One acc = ops[0];
-  uint32_t cur = 1;
-  for (uint32_t i = 1; i < nops && e == cudaSuccess; ++i) {
-    const One dst = (i + 1 == nops) ? out : c.tmp(cur);
-    e = c.combine(ops[i], acc, dst, stream);
-    acc = dst;
-    cur = cur == 1 ? 2 : 1;
-  }
+  if (st->n_seen > stream_narrow_max_n(st->k)) return PSS_ERR_UNSUPPORTED;
+  // the wide root, then its counts in 32 bits (they fit: N + floor(N/k) < 2^32)
+  cudaError_t e = c.root(st->n_seen, c.wtmp(0), stream);
+  const WOne r = c.wtmp(0);
+  if (e == cudaSuccess)
+    e = narrow_launch(c.kb, c.k, 1, r.items, r.counts, r.errs, r.sizes, root->items, root->counts,
+                      root->errs, root->sizes, stream);
   return e == cudaSuccess ? PSS_OK : PSS_ERR_CUDA;
 }
 

@@ -234,6 +234,23 @@ __global__ void widen_kernel(const KT* items, const uint32_t* counts, const uint
 }
 
 template <typename KT>
+__global__ void narrow_kernel(const KT* wi, const uint64_t* wc, const uint64_t* we,
+                              const uint32_t* wsz, uint32_t k, uint32_t count, KT* items,
+                              uint32_t* counts, uint32_t* errs, uint32_t* sizes) {
+  const uint64_t total = (uint64_t)count * k;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(i / k);
+    if (i - (uint64_t)s * k < wsz[s]) {
+      items[i] = wi[i];
+      counts[i] = (uint32_t)wc[i];  // the caller guarantees the counts fit (N + N/k < 2^32)
+      errs[i] = (uint32_t)we[i];
+    }
+    if (i - (uint64_t)s * k == 0) sizes[s] = wsz[s];
+  }
+}
+
+template <typename KT>
 __global__ void __launch_bounds__(256) wide_prune_kernel(const KT* items, const uint64_t* counts,
                                                          const uint32_t* sizes, uint64_t thr,
                                                          KT* cand, uint32_t* n_cand) {
@@ -388,6 +405,22 @@ cudaError_t widen_launch(int kb, uint32_t k, uint32_t count, const void* items,
     widen_kernel<uint64_t><<<std::max(grid, 1), 256, 0, s>>>(
         static_cast<const uint64_t*>(items), counts, errs, sizes, k, count,
         static_cast<uint64_t*>(wi), wc, we, wsz);
+  return cudaGetLastError();
+}
+
+cudaError_t narrow_launch(int kb, uint32_t k, uint32_t count, const void* wi, const uint64_t* wc,
+                          const uint64_t* we, const uint32_t* wsz, void* items, uint32_t* counts,
+                          uint32_t* errs, uint32_t* sizes, cudaStream_t s) {
+  const uint64_t total = (uint64_t)count * k;
+  const int grid = std::max(1, (int)std::min<uint64_t>((total + 255) / 256, 4096));
+  if (kb == 4)
+    narrow_kernel<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(wi), wc, we, wsz, k,
+                                                  count, static_cast<uint32_t*>(items), counts,
+                                                  errs, sizes);
+  else
+    narrow_kernel<uint64_t><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(wi), wc, we, wsz, k,
+                                                  count, static_cast<uint64_t*>(items), counts,
+                                                  errs, sizes);
   return cudaGetLastError();
 }
 

@@ -145,11 +145,19 @@ def test_stream_validation_before_launch(pss):
     need = pss.pss_stream_workspace_bytes(pss.KEY_U32, 10, 100, 4)
     assert lib.pss_stream_init(by(st), 0, 10, 100, 4, dummy, need) == 0
     assert (st.k, st.leaf_len, st.batch_leaves, st.n_seen) == (10, 100, 4, 0)
-    # feeds: null chunk with len > 0; a stream longer than the u32 counters allow (R9)
+    # feeds: null chunk with len > 0; a stream longer than 2^63 items (64-bit counts above the
+    # blocks) or one whose length wraps
     assert lib.pss_stream_feed(by(st), None, 5, None) == 1
-    assert lib.pss_stream_feed(by(st), dummy, 1 << 32, None) == 2
-    assert lib.pss_stream_feed_host(by(st), dummy, (1 << 32) - 1, None) == 2
+    assert lib.pss_stream_feed(by(st), dummy, (1 << 63) + 1, None) == 2
+    assert lib.pss_stream_feed_host(by(st), dummy, (1 << 64) - 1, None) == 2
     assert st.n_seen == 0
+    # the narrow root is refused once N + N/k could exceed a u32 counter (R9); the wide one is not
+    big = pss._Stream.from_buffer_copy(st)
+    big.n_seen = 1 << 32
+    root = pss._Summ(0, 10, 1, 0x1000, 0x1000, 0x1000, 0x1000)
+    assert lib.pss_stream_root(by(big), by(root), None) == 2
+    assert lib.pss_stream_root_wide(by(big), by(pss._Summ(0, 11, 1, 0x1000, 0x1000, 0x1000,
+                                                             0x1000)), None) == 3
     # root: capacity mismatch
     root = pss._Summ(0, 11, 1, 0x1000, 0x1000, 0x1000, 0x1000)
     assert lib.pss_stream_root(by(st), by(root), None) == 3

@@ -140,3 +140,36 @@ def test_summarize_merge_large_k(pss):
     dA = torch.from_numpy(A).cuda()
     leaves, root = pss.pss_summarize_merge(dA, 5000, 6)
     assert root.host(0) == oracle.tree(oracle.leaves(A, 5000, 6, threads=6), 5000).as_tuples()
+
+
+def test_stream_beyond_2_32_items(pss):
+    """A stream of the paper's scale (29 10^9 items; the on-line setting of P:42): H's
+    2^29 keys fed 9 times, 4.83 10^9 items > 2^32, k = 100, leaves of 2^16. Above its blocks the
+    stream keeps 64-bit counts; its root equals the oracle's fixed tree over the 9 x 8192 leaves."""
+    w = inputs.WORKLOADS["H"]
+    A = w.generate()
+    k, LL, reps = 100, 1 << 16, 9
+    dA = torch.from_numpy(A).cuda()
+    st = pss.Stream(k, LL, pss.KEY_U32, batch_leaves=1024)
+    for _ in range(reps):
+        st.feed(dA)
+    root = st.root(wide=True)
+    torch.cuda.synchronize()
+    assert st.n_seen == reps * A.size > 1 << 32
+    with pytest.raises(pss.PssError):
+        st.root()  # u32 counts are refused past R9's bound
+    it, c, e, sz = oracle.leaves_padded(A, k, A.size // LL, threads=inputs.host_threads())
+    ref = oracle.tree_padded(*(np.concatenate([x] * reps) for x in (it, c, e, sz)), k,
+                             threads=inputs.host_threads())
+    assert root.host(0) == ref.as_tuples()
+
+
+def test_stream_count_beyond_2_32(pss):
+    """Closed form: one key repeated 9 x 2^29 times is the whole summary, with count 9 x 2^29
+    (> 2^32: a u32 counter would wrap) and error 0."""
+    x = 0xDEADBEEF
+    dA = torch.full((1 << 29,), x, dtype=torch.uint32, device="cuda")
+    st = pss.Stream(10, 1 << 16, pss.KEY_U32, batch_leaves=4096)
+    for _ in range(9):
+        st.feed(dA)
+    assert st.root(wide=True).host(0) == [(x, 9 << 29, 0)]
