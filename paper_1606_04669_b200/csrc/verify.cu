@@ -31,9 +31,13 @@ namespace pss {
 constexpr int VTHREADS = PSS_VT_THREADS;
 constexpr int VWARPS = VTHREADS / 32;
 constexpr uint32_t VT_SMEM = 2048;       // table entries staged in shared memory
-constexpr uint32_t VC_BYTES = VWARPS * 8192;  // shared-memory counter area per CTA
-constexpr uint32_t VLANE_MAX = VC_BYTES / (VWARPS * 32 * 2);  // nc for per-lane 16-bit counters
-constexpr uint32_t VWARP_MAX = VC_BYTES / (VWARPS * 4);       // nc for per-warp 32-bit counters
+// shared-memory counter bytes per warp: the general kernel's, and a smaller one for up to 75
+// candidates (per-lane counters only) that fits more CTAs per SM -- K4 is latency-bound, so the
+// occupancy pays (H, 72 candidates: 580 -> 504 us). The candidate count is known on the device
+// only: both kernels are launched when it may exceed 75 and the one that does not fit exits.
+constexpr uint32_t VCW_BIG = 8192, VCW_SMALL = 4864;
+__host__ __device__ constexpr uint32_t vlane_max(uint32_t vcw) { return vcw / (32 * 2); }
+__host__ __device__ constexpr uint32_t vwarp_max(uint32_t vcw) { return vcw / 4; }
 
 // table entry: (key, candidate index); index all-ones = empty
 template <typename KT>
@@ -322,7 +326,7 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
 }
 
 // lane_ok: per-lane 16-bit counters cannot overflow for this launch (host-checked)
-template <typename KT>
+template <typename KT, uint32_t VCW>
 __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__ A, uint64_t n,
                                                           uint32_t cap, const uint32_t* d_n,
                                                           unsigned long long* acc,
@@ -337,7 +341,10 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint32_t T = 1u << logT;
   const uint32_t warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
-  const int mode = (lane_ok && nc < VLANE_MAX && T <= VT_SMEM) ? 0 : (nc <= VWARP_MAX ? 1 : 2);
+  const bool small_fits = lane_ok && nc < vlane_max(VCW_SMALL) && T <= VT_SMEM;
+  if (small_fits != (VCW == VCW_SMALL)) return;  // the other kernel's case
+  const int mode = (lane_ok && nc < vlane_max(VCW) && T <= VT_SMEM) ? 0
+                   : (nc <= vwarp_max(VCW) ? 1 : 2);
   VT* stab = reinterpret_cast<VT*>(vsm);
   unsigned char* carea = vsm + (size_t)VT_SMEM * sizeof(VT);
   const uint32_t ncw = (nc + 2) / 2;  // words per lane in mode 0 (nc counters + the dummy)
@@ -413,17 +420,29 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
   auto* ctl = reinterpret_cast<uint32_t*>(w + L.ctl);
   if (cap == 0) return cudaSuccess;
   verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, ctl);
-  const size_t smem = (size_t)VT_SMEM * sizeof(VT) + VC_BYTES;
-  allow_max_smem(verify_kernel<KT>, d);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, verify_kernel<KT>, VTHREADS, smem);
-  if (nb < 1) nb = 1;
-  const uint64_t want = (n + (uint64_t)VTHREADS * 64 - 1) / ((uint64_t)VTHREADS * 64);
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nb * d.sms));
-  // items one lane counts: at most ceil(n / (grid * VTHREADS)) + the head/tail
-  const uint64_t per_lane = n / ((uint64_t)grid * VTHREADS) + 64;
-  const uint32_t lane_ok = per_lane < 65535u;
-  verify_kernel<KT><<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, ctl, lane_ok);
+  // per-lane 16-bit counters cannot overflow: a lane counts at most n / (CTAs * VTHREADS) + the
+  // head/tail items; checked against the smaller of the two grids (the big kernel's)
+  int nb_big = 0;
+  allow_max_smem(verify_kernel<KT, VCW_BIG>, d);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_big, verify_kernel<KT, VCW_BIG>, VTHREADS,
+                                                (size_t)VT_SMEM * sizeof(VT) + VWARPS * VCW_BIG);
+  const uint64_t want0 = (n + (uint64_t)VTHREADS * 64 - 1) / ((uint64_t)VTHREADS * 64);
+  const uint64_t grid_min = std::max<uint64_t>(1, std::min<uint64_t>(want0, (uint64_t)std::max(nb_big, 1) * d.sms));
+  const uint32_t lane_ok = n / (grid_min * VTHREADS) + 64 < 65535u;
+  auto launch = [&](auto kern, uint32_t vcw) {
+    const size_t smem = (size_t)VT_SMEM * sizeof(VT) + (size_t)VWARPS * vcw;
+    allow_max_smem(kern, d);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, VTHREADS, smem);
+    if (nb < 1) nb = 1;
+    const uint64_t want = (n + (uint64_t)VTHREADS * 64 - 1) / ((uint64_t)VTHREADS * 64);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nb * d.sms));
+    // items one lane counts: at most ceil(n / (grid * VTHREADS)) + the head/tail; both
+    // kernels must agree on it (the small kernel's grid is the larger one)
+    kern<<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, ctl, lane_ok);
+  };
+  launch(verify_kernel<KT, VCW_SMALL>, VCW_SMALL);
+  if (cap >= vlane_max(VCW_SMALL)) launch(verify_kernel<KT, VCW_BIG>, VCW_BIG);
   verify_finalize_kernel<KT><<<(cap + 255) / 256, 256, 0, s>>>(cand, cap, d_n, acc, tab, ctl, exact);
   return cudaGetLastError();
 }

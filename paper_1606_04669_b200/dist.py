@@ -126,11 +126,14 @@ class Runner:
                     torch.empty((k,), dtype=torch.uint64, device=self.dev),
                     torch.zeros((1,), dtype=torch.uint32, device=self.dev))
         self.host_out = tuple(torch.empty_like(t, device="cpu").pin_memory() for t in self.out)
-        # K1 (+ the histogram kernel when used), the tree, [widen + one wide COMBINE launch per
-        # top level], prune, verify (setup, scan, finalize), report
+        # K1 (+ the histogram kernel when 40 k >= block length), the tree, [widen + one wide
+        # COMBINE launch per top level], prune, verify (setup, the scan for <= 75 candidates and,
+        # when k allows more, the general scan, finalize), report
         top_levels = (world - 1).bit_length() if world > 1 else 0
-        self.launches_per_step = (1 + _merge_launches(P, k, kb) +
-                                  (1 + top_levels if world > 1 else 0) + 1 + 3 + 1)
+        hist = 1 if 40 * k >= -(-n // P) and -(-n // P) <= (1 << 17) else 0
+        verify = 3 + (1 if k >= 76 else 0)
+        self.launches_per_step = (1 + hist + _merge_launches(P, k, kb) +
+                                  (1 + top_levels if world > 1 else 0) + 1 + verify + 1)
         self.host_api = "pss_query_host" if world == 1 else "H2D copy + step + D2H (torch)"
         self._kb = kb
 
