@@ -368,6 +368,19 @@ pss_status pss_merge_hybrid(const pss_summaries* leaves, uint32_t T, pss_summari
 pss_status pss_read_probe(const void* d_A, uint64_t n, pss_key_type kt, uint32_t* d_out,
                           cudaStream_t stream);
 
+/*
+ * pss_leaf_kernels -- which kernels pss_summarize (and every call that summarizes leaves) runs for
+ * this shape, as bit flags: PSS_LEAF_K1 (the per-warp batched rule, csrc/summarize.cu),
+ * PSS_LEAF_K1E (the per-CTA epoch formulation, csrc/epoch.cu; u32 keys, 64 <= k <= 2048),
+ * PSS_LEAF_K1H (the histogram kernel in front, for blocks with at most k distinct keys; blocks it
+ * gives up on go to K1E or K1). All of them produce the leaves of Alg. 1 l.5 bit for
+ * bit; this query only reports the routing (tests and tools). 0 for an invalid shape. Host only.
+ */
+#define PSS_LEAF_K1 1
+#define PSS_LEAF_K1E 2
+#define PSS_LEAF_K1H 4
+int pss_leaf_kernels(uint64_t n, uint32_t k, uint32_t P, pss_key_type kt);
+
 /* Human-readable name of a status. */
 const char* pss_status_string(pss_status s);
 

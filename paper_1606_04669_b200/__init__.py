@@ -546,6 +546,23 @@ def pss_merge_hybrid(leaves: Summaries, T: int, out: Summaries | None = None,
     return out
 
 
+# ---- leaf kernel routing (include/pss.h: pss_leaf_kernels) ----------------------------------
+_lib.pss_leaf_kernels.argtypes = [_u64, _u32, _u32, _i32]
+_lib.pss_leaf_kernels.restype = _i32
+LEAF_K1, LEAF_K1E, LEAF_K1H = 1, 2, 4
+EXPORTED_SYMBOLS += ["pss_leaf_kernels"]
+__all__ += ["pss_leaf_kernels", "epoch_used", "LEAF_K1", "LEAF_K1E", "LEAF_K1H"]
+
+
+def pss_leaf_kernels(n: int, k: int, P: int, key_type: int) -> int:
+    """Bit flags of the kernels that summarize the leaves of this shape (LEAF_K1/K1E/K1H)."""
+    return int(_lib.pss_leaf_kernels(n, k, P, key_type))
+
+
+def epoch_used(n: int, k: int, P: int, key_bytes: int = 4) -> bool:
+    return bool(pss_leaf_kernels(n, k, P, KEY_U32 if key_bytes == 4 else KEY_U64) & LEAF_K1E)
+
+
 # ---- K6 read-bandwidth probe (include/pss.h: pss_read_probe) -------------------------------
 _lib.pss_read_probe.argtypes = [_vp, _u64, _i32, _vp, _vp]
 _lib.pss_read_probe.restype = _i32

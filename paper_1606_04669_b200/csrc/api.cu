@@ -173,7 +173,15 @@ pss_status pss_prune_wide(const pss_wsummaries* root, uint64_t n, void* d_cand,
                                        root->sizes, n, root->k, d_cand, d_n_cand, stream));
 }
 
-const char* pss_version(void) { return "pss-b200 0.1 (sm_100a)"; }
+const char* pss_version(void) { return "pss-b200 0.2 (sm_100a)"; }
+
+int pss_leaf_kernels(uint64_t n, uint32_t k, uint32_t P, pss_key_type kt) {
+  const int kb = key_bytes(kt);
+  if (!kb || k < 2 || P == 0) return 0;
+  const DevInfo d = dev_info();
+  return (epoch_used(n, kb, k, P, d) ? PSS_LEAF_K1E : PSS_LEAF_K1) |
+         (hist_used(n, kb, k, P, d) ? PSS_LEAF_K1H : 0);
+}
 
 size_t pss_workspace_bytes(int op, uint64_t n, uint32_t k, uint32_t P, pss_key_type kt) {
   const int kb = key_bytes(kt);

@@ -167,6 +167,13 @@ cudaError_t hist_launch(const void* A, uint64_t n, int kb, uint32_t k, uint32_t 
                         uint32_t* counts, uint32_t* errs, uint32_t* sizes, uint32_t* queue,
                         unsigned char* flagged, cudaStream_t s, const DevInfo& d, uint32_t r0,
                         uint32_t r1, uint32_t T, uint32_t* leaf_flags);
+// K1e (epoch.cu): the leaf summaries of u32 keys for 64 <= k <= 2048, one CTA per block, epoch by
+// epoch; K1 takes the shapes it does not cover
+bool epoch_used(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d);
+cudaError_t epoch_launch(const void* A, uint64_t n, uint32_t k, uint32_t P, void* items,
+                         uint32_t* counts, uint32_t* errs, uint32_t* sizes, uint32_t* queue,
+                         const unsigned char* skip, cudaStream_t s, const DevInfo& d, uint32_t r0,
+                         uint32_t r1, uint32_t T, uint32_t* leaf_flags, bool pdl);
 // wide.cu: summaries with 64-bit counts and errors (the tree above the leaves, > 2^31 items)
 size_t wide_combine_ws(int kb, uint32_t k, const DevInfo& d);
 size_t wide_merge_ws(int kb, uint32_t k, uint32_t count, const DevInfo& d);

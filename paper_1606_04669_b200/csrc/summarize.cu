@@ -838,6 +838,10 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
                                 r0, r1, T, leaf_flags);
     if (e != cudaSuccess) return e;
   }
+  if (epoch_used(n, kb, k, P, d))
+    return epoch_launch(A, n, k, P, items, counts, errs, sizes,
+                        reinterpret_cast<uint32_t*>(w + W.q) + qi, hist ? w + W.flagged : nullptr,
+                        s, d, r0, r1, T, leaf_flags, pdl);
   SumArgs a;
   a.skip = hist ? w + W.flagged : nullptr;
   a.A = A;

@@ -81,7 +81,7 @@ def resolve_H_bounds(vpts):
     return state, und, it
 
 
-def epoch_ss(A, k, stats=None):
+def epoch_ss(A, k, stats=None, snaps=None):
     L = len(A)
     keys = [None] * k
     cnt = [0] * k
@@ -145,6 +145,9 @@ def epoch_ss(A, k, stats=None):
             err[s] = m
         filled = max(filled, max((s + 1 for s, _, _ in new), default=0))
         index = {keys[s]: s for s in range(filled)}
+        if snaps is not None and full:
+            snaps.append(dict(m=m, ne=len(events), nv=len(vpts), nh=len(Hset),
+                              keys=list(keys), cnt=list(cnt), err=list(err)))
         if full:
             nm = min(cnt)
             assert nm == m + 1, (nm, m)
