@@ -151,6 +151,32 @@ namespace pss {
 #endif
 #define EPWATCH(cond, code, a0, a1, a2) EPREC(cond, code, a0, a1, a2)
 
+#ifdef PSS_EP_TIMING  // debug build: cycles per stage, summed over CTAs (tid 0's view)
+__device__ unsigned long long g_ep_tm[16];
+}  // namespace pss
+extern "C" int pss_debug_epoch_timing(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pss::g_ep_tm, sizeof(pss::g_ep_tm));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(pss::g_ep_tm, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+namespace pss {
+#define EPTM(i)                                         \
+  do {                                                  \
+    if (tid == 0) {                                     \
+      const long long _n = clock64();                   \
+      atomicAdd(&g_ep_tm[i], (unsigned long long)(_n - tm0)); \
+      tm0 = _n;                                         \
+    }                                                   \
+  } while (0)
+#else
+#define EPTM(i) \
+  do {          \
+  } while (0)
+#endif
+
 // block barrier entered by converged warps only: bar.sync counts a warp as arrived when any of its
 // lanes executes it, so lanes that diverged (the U-table claim loop) must reconverge first
 __device__ __forceinline__ void ep_bar() {
@@ -184,6 +210,9 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
   __shared__ uint32_t s_ovf[EP_OVF];  // keys whose two buckets were full in a rebuild
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
   const uint32_t ltm = lanemask_lt();
+#ifdef PSS_EP_TIMING
+  long long tm0 = clock64();
+#endif
 
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);
   uint32_t* cw = reinterpret_cast<uint32_t*>(smem + a.o_cw);     // count | err << cb
@@ -206,7 +235,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
   const uint4* tk4 = reinterpret_cast<const uint4*>(tk);
   const uint2* ts2 = reinterpret_cast<const uint2*>(ts);
 
-  const uint32_t k = a.k, UC = a.UC, cb = a.cb;
+  const uint32_t k = a.k, UC = a.UC, UB = a.UC / 4, cb = a.cb;
 #ifdef PSS_EP_NBDIV  // debug: a crowded index (frequent rebuild overflows)
   const uint32_t NB = max(1u, a.NB * 2 / PSS_EP_NBDIV);
 #else
@@ -274,6 +303,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
     auto epoch_end = [&](bool full) {
       ep_bar();  // events, V list and occurrence counts of the epoch are complete
       EPHB(10);
+      EPTM(4);
       const uint32_t ne = ecount;
       const uint32_t nvv = full ? s_misc[1] : nv;
       // (1) warp 0: which V events hit (closed form, in time order, 32 at a time). A hit marks
@@ -384,6 +414,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
       }
       ep_bar();
       EPHB(11);
+      EPTM(5);
       const uint32_t nmiss = ne - s_misc[4];
       EPCHK(s_misc[4] <= nvv && nvv <= ne, 9, s_misc[4], nvv, ne);
       // (2) misses in time order: event i's rank is i minus the hits before it
@@ -395,6 +426,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
         if (code != EP_HIT) ml[EPIDX(i - hcp[base >> 5] - __popc(hm & ltm), k, 109)] = (uint16_t)code;
       }
       ep_bar();
+      EPTM(6);
       // (3) pops: the j-th unhit member (slot order) takes miss j: key, count m + occurrences,
       // error m. Sources are the U table or the V misses' copies, so slots are written in place.
       for (uint32_t s = tid; s < KW * 32; s += NT) {
@@ -422,10 +454,6 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
       }
       if (size < k) size = full ? k : nmiss;  // the fill epoch pops slots 0, 1, ... in order
       ep_bar();
-#ifdef PSS_EP_RESET_TABLES  // experiment: clear the U table at every epoch end
-      if (full)
-        for (uint32_t i = tid; i < UC; i += NT) ut[i] = EP_UEMPTY;
-#endif
 #ifdef PSS_EP_DUMP
       if (r == 0 && full && eseq - 1 < EP_DUMP_E) {
         unsigned* dd = g_ep_dump[eseq - 1];
@@ -442,6 +470,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
       }
 #endif
       if (!full) return;
+      EPTM(7);
       // (4) level m + 1: members = slots with count m + 1; rebuild the index with member flags
       ++m;
       ++eseq;
@@ -548,6 +577,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
       }
       ep_bar();
       b = s_misc[3];
+      EPTM(8);
       EPWATCH(b >= 1, 3, ne, nvv, 0);
       ecount = 0;
       nv = 0;
@@ -584,6 +614,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
         EPWATCH(++npass < 600, 12, q, npass, b);
         if (npass >= 600) break;
 #endif
+        EPTM(0);
         // (1) classify against the epoch-start index; first times of V and U keys
         uint32_t cls[R], id[R];  // cls 0: S, 1: V, 2: U; id: slot or U entry
 #pragma unroll
@@ -608,55 +639,102 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
           id[j] = e & 0x7fffu;
           cls[j] = e == EP_E16 ? 2u : (e >> 15);
         }
+        EPTM(9);
+#ifdef PSS_EP_TIMING
+        if (tid == 0) atomicAdd(&g_ep_tm[12], 1ull);
+        if (lane == 0) {
+          uint32_t nu = 0;
+          for (int j = 0; j < R; ++j) nu += __popc(__ballot_sync(1u, 0) | 0);
+          (void)nu;
+        }
+#endif
+        const uint32_t estamp = eseq << 20;
+        uint32_t utodo = 0;  // rows whose U key still has to be found or claimed
 #pragma unroll
         for (int j = 0; j < R; ++j) {
           const uint32_t t = q + j * NT + tid;
           if (((pend >> j) & 1u) && cls[j] == 1)
-            atomicMax(&vft[EPIDX(id[j], k, 118)], (eseq << 20) | (0xfffffu - t));
-          // U keys: find or claim their entry of the epoch's U table. The loop is warp-uniform
-          // (one probe step per lane per trip) so that the warp reaches the barrier converged.
-          bool todo = ((pend >> j) & 1u) && cls[j] == 2;
-          const uint32_t xx = x[j];
-          const unsigned long long mine = ((unsigned long long)xx << 32) | (eseq << 20) | t;
-          uint32_t h = ep_uhash(xx, UC);
-          unsigned long long e = todo ? ut[h] : 0ull;
-#if defined(PSS_EP_DEBUG) || defined(PSS_EP_GUARD)
-          uint32_t probes = 0;
-#endif
-          while (__any_sync(PSS_FULL, todo)) {
-            if (todo) {
-              if ((((uint32_t)e >> 20) & 0xfffu) != eseq) {  // empty or stale: claim it
-                const unsigned long long old = atomicCAS(&ut[h], e, mine);
-                if (old == e) {
-                  uo[h] = 0;
-                  todo = false;
-                } else {
-                  e = old;  // taken meanwhile: look at it again
-                }
-              } else if ((uint32_t)(e >> 32) == xx) {
-                // earlier time: lower the entry with plain 64-bit CAS (the same atomic unit as
-                // the claims; the entry only ever decreases)
-                while ((uint32_t)e > (uint32_t)mine) {
-                  const unsigned long long old = atomicCAS(&ut[h], e, mine);
-                  if (old == e) break;
-                  e = old;
-                }
-                todo = false;
-              } else {
-                h = h + 1 == UC ? 0u : h + 1;
-                e = ut[h];
-#if defined(PSS_EP_DEBUG) || defined(PSS_EP_GUARD)
-                if (++probes >= UC) {
-                  EPWATCH(false, 1, xx, t, UC);
-                  todo = false;
-                }
-#endif
-              }
-            }
+            atomicMax(&vft[EPIDX(id[j], k, 118)], estamp | (0xfffffu - t));
+          if (((pend >> j) & 1u) && cls[j] == 2) {
+            utodo |= 1u << j;
+            id[j] = ep_uhash(x[j], UB);  // the bucket to look in next
           }
-          if (cls[j] == 2) id[j] = h;
         }
+        // U keys: find or claim their entry in the epoch's U table (buckets of 4 64-bit entries
+        // key << 32 | eseq << 20 | t, read whole; linear probing over buckets). One warp-uniform
+        // loop serves every row, one probe per lane per trip, so that warps reach the barrier
+        // converged. Entries change only by 64-bit CAS (claims, and lowering the first time).
+#if defined(PSS_EP_DEBUG) || defined(PSS_EP_GUARD)
+        uint32_t probes = 0;
+#endif
+        while (__any_sync(PSS_FULL, utodo != 0)) {
+#ifdef PSS_EP_TIMING
+          if (tid == 0) atomicAdd(&g_ep_tm[11], 1ull);
+#endif
+          if (utodo) {
+            const uint32_t j = __ffs(utodo) - 1;
+            uint32_t xx = x[0], ub = id[0];
+#pragma unroll
+            for (int jj = 1; jj < R; ++jj)
+              if (j == (uint32_t)jj) {
+                xx = x[jj];
+                ub = id[jj];
+              }
+            const uint32_t lo_m = estamp | (q + j * NT + tid);
+            const uint4 w01 = reinterpret_cast<const uint4*>(ut)[2 * ub];
+            const uint4 w23 = reinterpret_cast<const uint4*>(ut)[2 * ub + 1];
+            // entry w = (lo, hi) = (eseq << 20 | t, key): current iff (lo ^ estamp) < 2^20;
+            // t = 2^20 - 1 marks an entry being claimed (its key not yet written)
+            const uint32_t busyv = estamp | 0xfffffu;
+            const uint32_t cur = ((w01.x ^ estamp) < 0x100000u ? 1u : 0u) |
+                                 ((w01.z ^ estamp) < 0x100000u ? 2u : 0u) |
+                                 ((w23.x ^ estamp) < 0x100000u ? 4u : 0u) |
+                                 ((w23.z ^ estamp) < 0x100000u ? 8u : 0u);
+            const uint32_t busy = (w01.x == busyv ? 1u : 0u) | (w01.z == busyv ? 2u : 0u) |
+                                  (w23.x == busyv ? 4u : 0u) | (w23.z == busyv ? 8u : 0u);
+            const uint32_t hit = cur & ~busy &
+                                 ((w01.y == xx ? 1u : 0u) | (w01.w == xx ? 2u : 0u) |
+                                  (w23.y == xx ? 4u : 0u) | (w23.w == xx ? 8u : 0u));
+            // the way to use: x's entry, else (no claim in flight here) the first free one
+            const uint32_t sel = hit ? hit : (busy ? 0u : (~cur & 15u));
+            bool done = false;
+            uint32_t h = 0;
+            if (sel) {
+              const uint32_t w = __ffs(sel) - 1;
+              h = 4 * ub + w;
+              uint32_t elo = w01.x;
+              elo = w == 1 ? w01.z : elo;
+              elo = w == 2 ? w23.x : elo;
+              elo = w == 3 ? w23.z : elo;
+              uint32_t* const lop = reinterpret_cast<uint32_t*>(ut) + 2 * h;
+              if (hit) {  // found: keep the earliest time (native 32-bit min on the low word)
+                if (elo > lo_m) atomicMin(lop, lo_m);
+                done = true;
+              } else if (atomicCAS(lop, elo, busyv) == elo) {  // claimed: publish key and time
+                *reinterpret_cast<uint2*>(lop) = make_uint2(lo_m, xx);
+                uo[h] = 0;
+                done = true;
+              }  // else: raced, look at the bucket again
+            } else if (busy) {
+              // a claim in flight in this bucket (maybe of x): look again
+            } else {  // bucket full of other keys of this epoch: next bucket
+              ub = ub + 1 == UB ? 0u : ub + 1;
+#if defined(PSS_EP_DEBUG) || defined(PSS_EP_GUARD)
+              if (++probes >= UB) {
+                EPWATCH(false, 1, xx, q + j * NT + tid, UB);
+                done = true;
+              }
+#endif
+            }
+#pragma unroll
+            for (int jj = 0; jj < R; ++jj)
+              if (j == (uint32_t)jj) id[jj] = done ? h : ub;
+            if (done) utodo &= utodo - 1;
+          }
+        }
+        EPTM(10);
         ep_bar();
+        EPTM(1);
         // (2) events: first occurrences of V and U keys; per-warp counts for the time-order scan
         uint32_t evb[R], vb[R];
 #pragma unroll
@@ -672,6 +750,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
           if (lane == 0) cbuf[j * NW + wid] = __popc(evb[j]) | (__popc(vb[j]) << 16);
         }
         ep_bar();
+        EPTM(2);
         // (3) time-order ranks (a shuffle scan of the R * NW counts); items up to the epoch's
         // b-th event are applied
         const uint32_t cv = lane < R * NW ? cbuf[lane] : 0u;
@@ -717,6 +796,7 @@ __global__ void __launch_bounds__(NT, EP_MIN_CTAS) ep_kernel(const EpArgs a) {
             }
           }
         }
+        EPTM(3);
         if (!ended) {
           ecount += tot_e;
           nv += tot_v;
@@ -796,7 +876,8 @@ static EpPlan ep_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   p.NB = std::max<uint32_t>(1, (k + 1) / 2);
 #endif
   const uint32_t SW = EP_NT * EP_R;
-  p.UC = (k + SW) + (k + SW) / 3 + 4;  // distinct U keys of an epoch <= b + one window
+  // distinct U keys of an epoch <= b + one window; buckets of 4 entries at load <= ~0.7
+  p.UC = 4 * ((((k + SW) * 10 + 6) / 7 + 3) / 4);
   if (p.UC >= EP_VFLAG) return p;
   Bump b;
   b.al = 16;
@@ -807,7 +888,9 @@ static EpPlan ep_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   p.o_tk = (uint32_t)b.take<uint32_t>(4 * (size_t)p.NB);
   p.o_ts = (uint32_t)b.take<uint16_t>(4 * (size_t)p.NB);
   p.o_fill = (uint32_t)b.take<uint32_t>((p.NB + 1) / 2);
-  p.o_ut = (uint32_t)b.take<unsigned long long>(p.UC);
+  b.al = 32;
+  p.o_ut = (uint32_t)b.take<unsigned long long>(p.UC);  // 32-byte buckets
+  b.al = 16;
   p.o_uo = (uint32_t)b.take<uint32_t>(p.UC);
   p.o_ev = (uint32_t)b.take<uint16_t>(k);
   p.o_vl = (uint32_t)b.take<uint16_t>(k);
