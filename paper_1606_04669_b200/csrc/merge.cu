@@ -787,9 +787,120 @@ static bool dispatch_comb(const CombArgs& a, int grid, const MPlan& p, cudaStrea
   return false;
 }
 
+// ---- canonical order (R5: count descending, then item ascending) of one summary by ranks, for
+// summaries too large for a CTA's shared memory (k beyond ~2000). A summary holds distinct
+// items, so the canonical order is a permutation: the rank of counter i is the number of
+// counters before it; a 2-D grid (counter tiles x slices of the summary) adds partial ranks,
+// then each counter is written at its rank. Replaces the single-CTA bitonic sort over global
+// scratch (C4-k20000: 2.2 ms for the root).
+constexpr int RK_NT = 256, RK_SLICE = 1024;
+template <typename KT>
+__global__ void __launch_bounds__(RK_NT) rank_partial_kernel(const KT* items,
+                                                             const uint32_t* counts,
+                                                             const uint32_t* size_p,
+                                                             uint32_t* rank) {
+  __shared__ KT sx[RK_NT];
+  __shared__ uint32_t sc[RK_NT];
+  const uint32_t size = *size_p;
+  const uint32_t i = blockIdx.x * RK_NT + threadIdx.x;
+  const uint32_t j0 = blockIdx.y * RK_SLICE, j1 = min(size, j0 + RK_SLICE);
+  if (blockIdx.x * RK_NT >= size || j0 >= size) return;
+  const bool act = i < size;
+  const uint32_t c = act ? counts[i] : 0u;
+  const KT x = act ? items[i] : KT(0);
+  uint32_t r = 0;
+  for (uint32_t t = j0; t < j1; t += RK_NT) {
+    __syncthreads();
+    if (t + threadIdx.x < j1) {
+      sx[threadIdx.x] = items[t + threadIdx.x];
+      sc[threadIdx.x] = counts[t + threadIdx.x];
+    }
+    __syncthreads();
+    const uint32_t m = min((uint32_t)RK_NT, j1 - t);
+    for (uint32_t u = 0; u < m; ++u) r += canon_before(sc[u], sx[u], c, x);
+  }
+  if (act && r) atomicAdd(&rank[i], r);
+}
+template <typename KT>
+__global__ void rank_scatter_kernel(const KT* items, const uint32_t* counts, const uint32_t* errs,
+                                    const uint32_t* size_p, const uint32_t* rank, KT* oi,
+                                    uint32_t* oc, uint32_t* oe, uint32_t* osize) {
+  const uint32_t size = *size_p;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *osize = size;
+  if (i >= size) return;
+  const uint32_t r = rank[i];
+  oi[r] = items[i];
+  oc[r] = counts[i];
+  oe[r] = errs[i];
+}
+// in = one summary (<= k counters), out = the same counters in canonical order; rank: k words
+static cudaError_t canon_rank_sort(int kb, uint32_t k, NodeRef in, NodeOut out, uint32_t* rank,
+                                   cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(rank, 0, (size_t)k * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((k + RK_NT - 1) / RK_NT, (k + RK_SLICE - 1) / RK_SLICE);
+  const int sg = (int)((k + 255) / 256);
+  if (kb == 4) {
+    rank_partial_kernel<uint32_t><<<grid, RK_NT, 0, s>>>(
+        static_cast<const uint32_t*>(in.items), in.counts, in.sizes, rank);
+    rank_scatter_kernel<uint32_t><<<sg, 256, 0, s>>>(
+        static_cast<const uint32_t*>(in.items), in.counts, in.errs, in.sizes, rank,
+        static_cast<uint32_t*>(out.items), out.counts, out.errs, out.sizes);
+  } else {
+    rank_partial_kernel<uint64_t><<<grid, RK_NT, 0, s>>>(
+        static_cast<const uint64_t*>(in.items), in.counts, in.sizes, rank);
+    rank_scatter_kernel<uint64_t><<<sg, 256, 0, s>>>(
+        static_cast<const uint64_t*>(in.items), in.counts, in.errs, in.sizes, rank,
+        static_cast<uint64_t*>(out.items), out.counts, out.errs, out.sizes);
+  }
+  return cudaGetLastError();
+}
+// bytes of the unsorted-root staging + ranks (large-k path only)
+static size_t rank_tmp_bytes(int kb, uint32_t k) {
+  return align_up((size_t)k * kb, 256) + 2 * align_up((size_t)k * 4, 256) + 256 +
+         align_up((size_t)k * 4, 256);
+}
+struct RankTmp {
+  NodeOut node;
+  uint32_t* rank;
+};
+static RankTmp rank_tmp(void* base, int kb, uint32_t k) {
+  unsigned char* w = static_cast<unsigned char*>(base);
+  RankTmp t;
+  size_t o = 0;
+  t.node.items = w + o;
+  o += align_up((size_t)k * kb, 256);
+  t.node.counts = reinterpret_cast<uint32_t*>(w + o);
+  o += align_up((size_t)k * 4, 256);
+  t.node.errs = reinterpret_cast<uint32_t*>(w + o);
+  o += align_up((size_t)k * 4, 256);
+  t.node.sizes = reinterpret_cast<uint32_t*>(w + o);
+  o += 256;
+  t.rank = reinterpret_cast<uint32_t*>(w + o);
+  return t;
+}
+
+static size_t scratch_bytes(int kb, uint32_t k, const DevInfo& d);
 static cudaError_t combine_run(int kb, uint32_t k, CombArgs a, void* ws, cudaStream_t s,
                                const DevInfo& d) {
   MPlan p = m_plan(kb, k, d);
+  if (p.g && a.sort_out && a.nblocks == 1) {
+    // large k: the set by the level kernel's radix selection, the order by ranks (the staging
+    // node and ranks follow the COMBINE scratch in ws)
+    const RankTmp t = rank_tmp(static_cast<unsigned char*>(ws) + align_up(scratch_bytes(kb, k, d), 256), kb, k);
+    const NodeOut final_out = a.o;
+    if (a.canon_single && a.nright == 0) {  // COMBINE(S, empty): S itself, reordered
+      return canon_rank_sort(kb, k, a.a, final_out, t.rank, s);
+    }
+    a.o = t.node;
+    a.sort_out = 0;
+    a.canon_single = 0;
+    cudaError_t e = combine_run(kb, k, a, ws, s, d);
+    if (e != cudaSuccess) return e;
+    return canon_rank_sort(kb, k, NodeRef{t.node.items, t.node.counts, t.node.errs, t.node.sizes},
+                           final_out, t.rank, s);
+  }
   fill_comb_args(a, kb, k, p, ws);
   if (a.nblocks == 0) return cudaSuccess;
   const int grid = (int)std::min<uint32_t>(a.nblocks, (uint32_t)p.grid_cap);
@@ -808,7 +919,8 @@ static size_t scratch_bytes(int kb, uint32_t k, const DevInfo& d) {
 }
 
 size_t combine_ws(int kb, uint32_t k, uint32_t, const DevInfo& d) {
-  return align_up(scratch_bytes(kb, k, d), 256) + 256;
+  return align_up(scratch_bytes(kb, k, d), 256) + 256 +
+         (m_plan(kb, k, d).g ? rank_tmp_bytes(kb, k) : 0);
 }
 
 cudaError_t combine_launch(int kb, uint32_t k, uint32_t count, const void* a_items,
@@ -872,7 +984,8 @@ static TreeWs tree_ws(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
   w.sizes = b.take<uint32_t>(nn);
   w.flags = b.take<uint32_t>(nn);
   w.queue = b.take<uint32_t>(1);
-  w.scratch = b.take<unsigned char>(scratch_bytes(kb, k, d));
+  w.scratch = b.take<unsigned char>(align_up(scratch_bytes(kb, k, d), 256) +
+                                     (m_plan(kb, k, d).g ? rank_tmp_bytes(kb, k) : 0));
   w.total = b.bytes();
   return w;
 }
