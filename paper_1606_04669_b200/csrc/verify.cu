@@ -28,6 +28,9 @@ namespace pss {
 #ifndef PSS_VT_U
 #define PSS_VT_U 4
 #endif
+#ifndef PSS_VT_FILTER
+#define PSS_VT_FILTER 0
+#endif
 constexpr int VTHREADS = PSS_VT_THREADS;
 constexpr int VWARPS = VTHREADS / 32;
 constexpr uint32_t VT_SMEM = 2048;       // table entries staged in shared memory
@@ -228,12 +231,25 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
                                             const typename VEnt<KT>::T* tab, uint32_t seed,
                                             uint32_t logT, uint32_t* lw, uint32_t* wc,
                                             unsigned long long* acc, uint64_t wid,
-                                            uint64_t nwarps, uint32_t nc) {
+                                            uint64_t nwarps, uint32_t nc, uint32_t fw = 0) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t ltm = lanemask_lt();
   uint32_t* const lwl = lw + lane;
 #if PSS_VT_EXP == 2 || PSS_VT_EXP == 3  // timing experiment: no table lookup
   auto look = [&](KT x) { return (uint32_t)x & 31u; };
+#elif PSS_VT_FILTER
+  // one-probe table behind a 1024-bit filter held one word per lane (bit b: an occupied entry
+  // whose index is b modulo 1024): a non-candidate usually costs a shuffle, not a table read
+  auto look = [&](KT x) -> uint32_t {
+    if (!PERF) return vlookup<KT>(tab, x, seed, logT, PERF);
+    uint32_t h1, h2;
+    vhash(x, seed, logT, h1, h2);
+    const uint32_t fb = h1 & 1023u;
+    const uint32_t w = __shfl_sync(PSS_FULL, fw, fb >> 5);
+    if (!((w >> (fb & 31u)) & 1u)) return 0xffffffffu;
+    const typename VEnt<KT>::T a = tab[h1];
+    return VEnt<KT>::key(a) == x ? VEnt<KT>::idx(a) : 0xffffffffu;
+  };
 #else
   auto look = [&](KT x) { return vlookup<KT>(tab, x, seed, logT, PERF); };
 #endif
@@ -267,7 +283,8 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
   // scalar head and tail (warp-uniform loops)
   for (uint64_t base = wid * 32; base < head; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    count1(i < head ? look(A[i]) : 0xffffffffu);
+    const uint32_t j = look(i < head ? A[i] : KT(0));  // every lane looks (shuffles inside)
+    count1(i < head ? j : 0xffffffffu);
   }
   const uint4* V = reinterpret_cast<const uint4*>(A + head);
   const uint64_t stride = nwarps * 32;
@@ -311,14 +328,18 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
     for (int u = 0; u < U; ++u) {
       const KT* xs = reinterpret_cast<const KT*>(&q[u]);
 #pragma unroll
-      for (uint32_t e = 0; e < E; ++e) count1(ok[u] ? look(xs[e]) : 0xffffffffu);
+      for (uint32_t e = 0; e < E; ++e) {
+        const uint32_t j = look(xs[e]);
+        count1(ok[u] ? j : 0xffffffffu);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) q[u] = nq[u];
   }
   for (uint64_t base = tail0 + wid * 32; base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
-    count1(i < n ? look(A[i]) : 0xffffffffu);
+    const uint32_t j = look(i < n ? A[i] : KT(0));
+    count1(i < n ? j : 0xffffffffu);
   }
 #if PSS_VT_EXP == 1 || PSS_VT_EXP == 3
   if (sink == 0x12345678u) acc[0] = sink;
@@ -363,8 +384,19 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
   const uint64_t wid = (uint64_t)blockIdx.x * VWARPS + warp;
   const uint64_t nwarps = (uint64_t)gridDim.x * VWARPS;
   if (mode == 0) {
+    uint32_t fw = 0;
+#if PSS_VT_FILTER
+    if (perf) {  // this lane's word of the filter: entries 32*lane + i and 1024 + 32*lane + i
+      const uint32_t lane = threadIdx.x & 31u;
+      for (uint32_t i = 0; i < 32; ++i) {
+        const uint32_t h = 32 * lane + i;
+        const bool occ = !VEnt<KT>::empty(stab[h]) || (h + 1024 < T && !VEnt<KT>::empty(stab[h + 1024]));
+        fw |= (occ ? 1u : 0u) << i;
+      }
+    }
+#endif
     if (perf)
-      verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc);
+      verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc, fw);
     else
       verify_scan<KT, 0, false>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc);
   } else {
