@@ -28,6 +28,12 @@ namespace pss {
 #ifndef PSS_VT_U
 #define PSS_VT_U 4
 #endif
+#ifndef PSS_VT_TAGPAD  // experiment: extra shared memory of the tagged kernel (fewer CTAs per SM)
+#define PSS_VT_TAGPAD 0
+#endif
+#ifndef PSS_VT_TAGMINB
+#define PSS_VT_TAGMINB 8
+#endif
 #ifndef PSS_VT_FILTER
 #define PSS_VT_FILTER 0
 #endif
@@ -89,20 +95,40 @@ __host__ __device__ static uint32_t v_logT(uint32_t nc) {
 }
 
 struct VLayout {
-  size_t acc, tab, ctl, total;
+  size_t acc, tab, tab32, ctl, total;
 };
 
 // perfect (collision-free, one probe) tables for up to PH_MAX distinct candidates
 constexpr uint32_t PH_MAX = 80;
 constexpr uint32_t PH_LOG = 11;  // 2048 entries
 constexpr int PH_TRIES = 64;
+// Tagged one-probe table for u32 keys (K4's common case: a few dozen candidates, per-lane
+// counters). ha = x * mult (mult odd: a bijection of the key); its top PH_LOG bits h are the entry,
+// so the low 21 bits identify the key inside it. Entry h holds (f ^ h) << 21 | ha's low bits, f the
+// key's counter code: e ^ ha is then f << 21 exactly for that key, and any other key leaves low
+// bits set. Rotated left by 11 this is f for a match and >= 2048 otherwise, so min(., PH_FDUMMY)
+// maps every non-candidate to the dummy counter without a compare. f = word | half << 10 of the
+// 16-bit counter [word][lane]; the dummy is the upper half of word 37, above every valid code
+// (at most 74 candidates). Empty entries hold the dummy's code with low bits 0. One 32-bit
+// shared-memory load and 12 instructions per key instead of a 64-bit load and 18.
+constexpr uint32_t PH_TAG_BITS = 32 - PH_LOG;
+constexpr uint32_t PH_TAG_MASK = (1u << PH_TAG_BITS) - 1u;
+constexpr uint32_t PH_TAG_MAXC = 74;
+constexpr uint32_t PH_FDUMMY = 1024u + 37u;
+__host__ __device__ constexpr uint32_t ph_fcode(uint32_t idx) {
+  return (idx >> 1) | ((idx & 1u) << 10);
+}
+static_assert(ph_fcode(PH_TAG_MAXC - 1) < PH_FDUMMY && PH_TAG_MAXC <= PH_MAX, "tagged entry");
+static_assert((PH_FDUMMY - 1024u + 1u) * 128u <= VCW_SMALL, "tagged counters fit the small area");
 
 static VLayout v_layout(int kb, uint32_t cap) {
   VLayout L;
   Bump b;
   L.acc = b.take<unsigned long long>(cap ? cap : 1);
   L.tab = b.take<unsigned char>(((size_t)1 << std::max(v_logT(cap), PH_LOG)) * (kb == 4 ? 8 : 16));
-  L.ctl = b.take<uint32_t>(4);  // [0] seed, [1] logT, [2] 1 = perfect table
+  L.tab32 = b.take<uint32_t>((size_t)1 << PH_LOG);  // tagged one-probe table (u32 keys)
+  // [0] seed, [1] logT, [2] 1 = perfect table, [3] multiplier of the tagged table (0 = none)
+  L.ctl = b.take<uint32_t>(4);
   L.total = b.bytes();
   return L;
 }
@@ -136,7 +162,7 @@ __device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT 
 template <typename KT>
 __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t* d_n,
                                     unsigned long long* acc, typename VEnt<KT>::T* tab,
-                                    uint32_t* ctl) {
+                                    uint32_t* tab32, uint32_t* ctl) {
   using VT = typename VEnt<KT>::T;
   const uint32_t nc = eff_count(cap, d_n);
   for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
@@ -165,6 +191,32 @@ __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t
           ctl[0] = seed;
           ctl[1] = PH_LOG;
           ctl[2] = 1;
+          ctl[3] = 0;
+        }
+        // the tagged table (u32 keys): its own multiplier search; ctl[3] = multiplier, 0 = none
+        if (sizeof(KT) == 4 && nc <= PH_TAG_MAXC) {
+          for (int t2 = 0; t2 < PH_TRIES; ++t2) {
+            const uint32_t mult = ((uint32_t)t2 * 0x9E3779B9u + 0x85EBCA6Bu) | 1u;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < TP / 32; i += blockDim.x) occ[i] = 0;
+            if (threadIdx.x == 0) clash = 0;
+            __syncthreads();
+            uint32_t ha = 0, hh = 0;
+            if (threadIdx.x < nc) {
+              ha = (uint32_t)cand[threadIdx.x] * mult;
+              hh = ha >> PH_TAG_BITS;
+              if (atomicOr(&occ[hh >> 5], 1u << (hh & 31)) & (1u << (hh & 31))) clash = 1;
+            }
+            __syncthreads();
+            if (clash) continue;
+            for (uint32_t e = threadIdx.x; e < TP; e += blockDim.x)
+              tab32[e] = (PH_FDUMMY ^ e) << PH_TAG_BITS;
+            __syncthreads();
+            if (threadIdx.x < nc)
+              tab32[hh] = ((ph_fcode(threadIdx.x) ^ hh) << PH_TAG_BITS) | (ha & PH_TAG_MASK);
+            if (threadIdx.x == 0) ctl[3] = mult;
+            break;
+          }
         }
         return;
       }
@@ -178,6 +230,7 @@ __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t
   __syncthreads();
   if (threadIdx.x != 0) return;
   ctl[2] = 0;
+  ctl[3] = 0;
   for (uint32_t seed = 0;; seed += 0x9E3779B9u) {
     if (seed)
       for (uint32_t h = 0; h < T; ++h) tab[h] = VEnt<KT>::none();
@@ -226,7 +279,7 @@ __device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v) {
 // out [cand / 2][lane] (a warp's adds hit 32 banks and never the same word), added with
 // red.shared so successive increments do not wait on each other; MODE 1: __match_any_sync groups
 // + per-warp 32-bit counters; MODE 2: groups + 64-bit global atomics. PERF: one-probe table.
-template <typename KT, int MODE, bool PERF>
+template <typename KT, int MODE, bool PERF, bool TAG = false>
 __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n,
                                             const typename VEnt<KT>::T* tab, uint32_t seed,
                                             uint32_t logT, uint32_t* lw, uint32_t* wc,
@@ -235,6 +288,8 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t ltm = lanemask_lt();
   uint32_t* const lwl = lw + lane;
+  const uint32_t lwl_addr = smem_u32(lwl);
+  (void)lwl_addr;
 #if PSS_VT_EXP == 2 || PSS_VT_EXP == 3  // timing experiment: no table lookup
   auto look = [&](KT x) { return (uint32_t)x & 31u; };
 #elif PSS_VT_FILTER
@@ -251,14 +306,28 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
     return VEnt<KT>::key(a) == x ? VEnt<KT>::idx(a) : 0xffffffffu;
   };
 #else
-  auto look = [&](KT x) { return vlookup<KT>(tab, x, seed, logT, PERF); };
+  auto look = [&](KT x) -> uint32_t {
+    if constexpr (TAG) {  // tagged 32-bit entries: the counter code, PH_FDUMMY for no candidate
+      const uint32_t ha = (uint32_t)x * seed;  // seed = the table's multiplier
+      const uint32_t e = reinterpret_cast<const uint32_t*>(tab)[ha >> PH_TAG_BITS];
+      return min(__funnelshift_l(e ^ ha, e ^ ha, PH_LOG), PH_FDUMMY);
+    } else {
+      return vlookup<KT>(tab, x, seed, logT, PERF);
+    }
+  };
 #endif
 #if PSS_VT_EXP == 1 || PSS_VT_EXP == 3  // timing experiment: no counting
   uint32_t sink = 0;
   auto count1 = [&](uint32_t j) { sink += j; };
 #else
   auto count1 = [&](uint32_t j) {
-    if (MODE == 0) {  // no candidate: counted in the dummy counter nc (no branch)
+    if (TAG) {  // j = counter code: word | half << 10 (0xffffffff: an item outside A)
+      const uint32_t f = min(j, PH_FDUMMY);
+      uint32_t ad;  // lwl + word * 32 words, as one multiply-add
+      asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(ad) : "r"(f & 1023u), "r"(lwl_addr));
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ad), "r"((f >> 10) * 65535u + 1u)
+                   : "memory");
+    } else if (MODE == 0) {  // no candidate: counted in the dummy counter nc (no branch)
       const uint32_t jj = min(j, nc);
       red_shared_add(lwl + (jj >> 1) * 32, 1u << ((jj & 1u) << 4));
     } else {
@@ -346,32 +415,52 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
 #endif
 }
 
-// lane_ok: per-lane 16-bit counters cannot overflow for this launch (host-checked)
+// lane_ok: per-lane 16-bit counters cannot overflow for this launch (host-checked).
+// The VCW_SMALL kernel of u32 keys is the tagged one (TAG): it takes the launches whose candidates
+// sit in a one-probe table (perf) and fit per-lane counters; everything else goes to VCW_BIG.
 template <typename KT, uint32_t VCW>
-__global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__ A, uint64_t n,
+struct VKern {
+  static constexpr bool TAG = VCW == VCW_SMALL && sizeof(KT) == 4;
+  static constexpr size_t TAB_BYTES =
+      TAG ? ((size_t)4 << PH_LOG) : (size_t)VT_SMEM * sizeof(typename VEnt<KT>::T);
+  static constexpr size_t SMEM = TAB_BYTES + (size_t)VWARPS * VCW + (TAG ? PSS_VT_TAGPAD : 0);
+  static constexpr int MINB = TAG ? PSS_VT_TAGMINB : 1;  // CTAs per SM the registers must allow
+};
+
+template <typename KT, uint32_t VCW>
+__global__ void __launch_bounds__(VTHREADS, VKern<KT, VCW>::MINB) verify_kernel(const KT* __restrict__ A, uint64_t n,
                                                           uint32_t cap, const uint32_t* d_n,
                                                           unsigned long long* acc,
                                                           const typename VEnt<KT>::T* gtab,
+                                                          const uint32_t* gtab32,
                                                           const uint32_t* ctl, uint32_t lane_ok) {
   using VT = typename VEnt<KT>::T;
+  constexpr bool TAG = VKern<KT, VCW>::TAG;
   extern __shared__ __align__(16) unsigned char vsm[];
   const uint32_t nc = eff_count(cap, d_n);
   if (nc == 0) return;
-  const uint32_t seed = ctl[0], logT = ctl[1];
+  const uint32_t seed = TAG ? ctl[3] : ctl[0], logT = ctl[1];
   const bool perf = ctl[2] != 0;
   const uint32_t T = 1u << logT;
   const uint32_t warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
-  const bool small_fits = lane_ok && nc < vlane_max(VCW_SMALL) && T <= VT_SMEM;
+  const bool small_fits =
+      sizeof(KT) == 4 ? lane_ok && perf && ctl[3] != 0 && nc <= PH_TAG_MAXC
+                      : lane_ok && nc < vlane_max(VCW_SMALL) && T <= VT_SMEM;
   if (small_fits != (VCW == VCW_SMALL)) return;  // the other kernel's case
   const int mode = (lane_ok && nc < vlane_max(VCW) && T <= VT_SMEM) ? 0
                    : (nc <= vwarp_max(VCW) ? 1 : 2);
   VT* stab = reinterpret_cast<VT*>(vsm);
-  unsigned char* carea = vsm + (size_t)VT_SMEM * sizeof(VT);
-  const uint32_t ncw = (nc + 2) / 2;  // words per lane in mode 0 (nc counters + the dummy)
+  unsigned char* carea = vsm + VKern<KT, VCW>::TAB_BYTES;
+  // words per lane in mode 0 (nc counters + the dummy; the tagged kernel's dummy is fixed)
+  const uint32_t ncw = TAG ? PH_FDUMMY - 1024u + 1u : (nc + 2) / 2;
   uint32_t* lw = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * ncw * 32;  // [cand/2][lane]
   uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;        // [cand]
   const bool tab_smem = T <= VT_SMEM;
+  if (TAG) {
+    for (uint32_t h = threadIdx.x; h < (1u << PH_LOG); h += VTHREADS)
+      reinterpret_cast<uint32_t*>(vsm)[h] = gtab32[h];
+  } else
   if (tab_smem)
     for (uint32_t h = threadIdx.x; h < T; h += VTHREADS) stab[h] = gtab[h];
   if (mode == 0)
@@ -395,7 +484,9 @@ __global__ void __launch_bounds__(VTHREADS) verify_kernel(const KT* __restrict__
       }
     }
 #endif
-    if (perf)
+    if (TAG)
+      verify_scan<KT, 0, true, TAG>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc, fw);
+    else if (perf)
       verify_scan<KT, 0, true>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc, fw);
     else
       verify_scan<KT, 0, false>(A, n, stab, seed, logT, lw, wc, acc, wid, nwarps, nc);
@@ -450,19 +541,19 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
   auto* acc = reinterpret_cast<unsigned long long*>(w + L.acc);
   auto* tab = reinterpret_cast<VT*>(w + L.tab);
   auto* ctl = reinterpret_cast<uint32_t*>(w + L.ctl);
+  auto* tab32 = reinterpret_cast<uint32_t*>(w + L.tab32);
   if (cap == 0) return cudaSuccess;
-  verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, ctl);
+  verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, tab32, ctl);
   // per-lane 16-bit counters cannot overflow: a lane counts at most n / (CTAs * VTHREADS) + the
   // head/tail items; checked against the smaller of the two grids (the big kernel's)
   int nb_big = 0;
   allow_max_smem(verify_kernel<KT, VCW_BIG>, d);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_big, verify_kernel<KT, VCW_BIG>, VTHREADS,
-                                                (size_t)VT_SMEM * sizeof(VT) + VWARPS * VCW_BIG);
+                                                VKern<KT, VCW_BIG>::SMEM);
   const uint64_t want0 = (n + (uint64_t)VTHREADS * 64 - 1) / ((uint64_t)VTHREADS * 64);
   const uint64_t grid_min = std::max<uint64_t>(1, std::min<uint64_t>(want0, (uint64_t)std::max(nb_big, 1) * d.sms));
   const uint32_t lane_ok = n / (grid_min * VTHREADS) + 64 < 65535u;
-  auto launch = [&](auto kern, uint32_t vcw) {
-    const size_t smem = (size_t)VT_SMEM * sizeof(VT) + (size_t)VWARPS * vcw;
+  auto launch = [&](auto kern, size_t smem) {
     allow_max_smem(kern, d);
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, VTHREADS, smem);
@@ -471,10 +562,13 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)nb * d.sms));
     // items one lane counts: at most ceil(n / (grid * VTHREADS)) + the head/tail; both
     // kernels must agree on it (the small kernel's grid is the larger one)
-    kern<<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, ctl, lane_ok);
+    kern<<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, tab32, ctl, lane_ok);
   };
-  launch(verify_kernel<KT, VCW_SMALL>, VCW_SMALL);
-  if (cap >= vlane_max(VCW_SMALL)) launch(verify_kernel<KT, VCW_BIG>, VCW_BIG);
+  launch(verify_kernel<KT, VCW_SMALL>, VKern<KT, VCW_SMALL>::SMEM);
+  // u32: the small kernel takes one-probe tables only, so the general one is always launched
+  // (it exits at once when the case is the small kernel's)
+  if (cap >= vlane_max(VCW_SMALL) || sizeof(KT) == 4)
+    launch(verify_kernel<KT, VCW_BIG>, VKern<KT, VCW_BIG>::SMEM);
   verify_finalize_kernel<KT><<<(cap + 255) / 256, 256, 0, s>>>(cand, cap, d_n, acc, tab, ctl, exact);
   return cudaGetLastError();
 }
