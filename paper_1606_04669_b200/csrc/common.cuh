@@ -160,6 +160,17 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
                              void* ws, cudaStream_t s, const DevInfo& d, uint32_t r0 = 0,
                              uint32_t r1 = 0xffffffffu, uint32_t qi = 0, uint32_t T = 1,
                              uint32_t* leaf_flags = nullptr, bool pdl = false);
+// K0 (hot.cu): the frequent keys of A[lo, hi) (u32) for K1's level-pinned bypass. `out`, HOT_WORDS
+// words in the workspace: [0] number of keys (0: none), [1] the table's multiplier, [2] their
+// occurrences in the sample, [3] sample size, [4..) the keys by rank, then a one-probe table of
+// 2^HOT_LOG entries: with ha = key * multiplier and h = ha >> 21, entry h holds (rank ^ h) << 21 |
+// ha's low 21 bits (rank HOT_NONE for an empty entry), so rotl(entry ^ ha, 11) is the key's rank
+// if it is in the table and a value >= HOT_MAX otherwise.
+constexpr uint32_t HOT_MAX = 64, HOT_LOG = 11, HOT_NONE = 127;
+constexpr uint32_t HOT_TAG_MASK = (1u << (32 - HOT_LOG)) - 1u;
+constexpr uint32_t HOT_WORDS = 4 + HOT_MAX + (1u << HOT_LOG);
+cudaError_t hot_sample_launch(const void* A, uint64_t lo, uint64_t hi, uint32_t* out, bool force,
+                              cudaStream_t s);
 // K1h (hist.cu): leaves of blocks with at most k distinct keys as exact histograms; the other
 // leaves are flagged (flagged[r] = 1) for K1
 bool hist_used(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d);

@@ -151,7 +151,7 @@ __device__ __forceinline__ uint32_t free_entry(ET e0, ET e1, ET e2, ET e3, uint3
 }
 
 struct SSLayout {
-  size_t keys, cnt, err, pos, bm, vic, T, total;
+  size_t keys, cnt, err, pos, bm, vic, hc, cq, cqp, T, total;
   uint32_t NB;
 };
 
@@ -168,7 +168,10 @@ static uint32_t ss_buckets(uint32_t k, double load) {
   return (uint32_t)std::max<double>(2.0, std::ceil(k / (2.0 * load)));
 }
 
-static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed, uint32_t NB) {
+// level-pinned bypass: the cold queue's capacity (items), a power of two >= 64
+constexpr uint32_t SS_CQ = 128;
+
+static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed, uint32_t NB, bool byp = false) {
   SSLayout L;
   const size_t KP = align_up(k, 32);
   L.NB = NB;
@@ -181,6 +184,10 @@ static SSLayout ss_layout(uint32_t k, int kb, int eb, bool packed, uint32_t NB) 
   L.pos = packed ? L.cnt : b.take<unsigned char>((size_t)k * (eb == 2 ? 2 : 4));
   L.bm = b.take<uint32_t>(KP / 32 + 2);
   L.vic = b.take<uint32_t>(32);
+  // bypass: counts of the pinned hot keys, the queue of cold items and their positions
+  L.hc = byp ? b.take<uint32_t>(HOT_MAX) : 0;
+  L.cq = byp ? b.take<unsigned char>((size_t)SS_CQ * kb) : 0;
+  L.cqp = byp ? b.take<uint16_t>(SS_CQ) : 0;  // positions < 2^16 (blocks of <= 2^16 items)
   L.T = b.take<unsigned char>((size_t)2 * L.NB * eb);
   L.total = b.bytes();  // a multiple of 16
   return L;
@@ -203,6 +210,8 @@ struct SumArgs {
   unsigned char* gstate;  // per-CTA state when it does not fit shared memory
   size_t gstride;
   size_t o_cnt, o_err, o_pos, o_bm, o_vic, o_T;
+  size_t o_hc, o_cq, o_cqp;
+  const uint32_t* hot;    // non-null: the frequent-key table of this launch's range (hot.cu)
   uint32_t NB;
   uint32_t cb;            // PACKED: count in the low cb bits, error above
   uint32_t sb, fmask;     // index entry layout
@@ -210,7 +219,9 @@ struct SumArgs {
 
 // SB, CB > 0: the index entry's slot bits and the counter word's count bits as compile-time
 // constants (shifts and masks become immediates and free registers: 4.5 % at H); 0: runtime
-template <typename KT, typename ET, bool GSTATE, bool PACKED, int SB = 0, int CB = 0>
+// BYP: the level-pinned bypass (below, "level-pinned bypass"), u32 keys with packed counters
+template <typename KT, typename ET, bool GSTATE, bool PACKED, int SB = 0, int CB = 0,
+          bool BYP = false>
 // 1-warp CTAs: __launch_bounds__(32) measured 12-15 % faster than any multi-warp bound (CTAs of
 // several independent warps, sharing the per-CTA reserved shared memory, lost more than the
 // extra residency gained)
@@ -266,6 +277,22 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   __syncwarp();
   uint32_t phasebits = 0;
   if (a.pdl) pdl_launch_dependents();
+  // level-pinned bypass: the launch's frequent keys (lane j keeps keys j and j + 32)
+  uint32_t nhot = 0, hseed = 0, hk0 = 0, hk1 = 0;
+  const uint32_t* htab = nullptr;
+  if constexpr (BYP) {
+    nhot = a.hot[0];
+    hseed = a.hot[1];
+    htab = a.hot + 4 + HOT_MAX;
+    hk0 = lane < nhot ? a.hot[4 + lane] : 0u;
+    hk1 = lane + 32 < nhot ? a.hot[4 + 32 + lane] : 0u;
+    if (nhot == 0) return;  // no table for this range: the plain kernel (launched next) runs
+  } else {
+    if (a.hot && a.hot[0] != 0) return;  // the bypass kernel (launched before) took the range
+  }
+  uint32_t* const hc = reinterpret_cast<uint32_t*>(st + a.o_hc);
+  KT* const cq = reinterpret_cast<KT*>(st + a.o_cq);
+  uint16_t* const cqp = reinterpret_cast<uint16_t*>(st + a.o_cqp);
 
   while (true) {
     uint32_t r = 0;
@@ -288,6 +315,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
     // ---- reset the summary
     for (uint32_t i = lane; i < NE; i += 32) T[i] = EMPTY;
     uint32_t size = 0, m = 0, bmcount = 0, cur = 0, seed = 0;
+    if constexpr (BYP) {
+      hc[lane] = 0;
+      hc[lane + 32] = 0;
+    }
     __syncwarp();
 
     auto new_level = [&]() {  // m = min count, B_m = {slots with count m}, cursor at slot 0
@@ -563,7 +594,122 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         SS_STAT(1, c);
         __syncwarp();
       }
-      if (size == k) new_level();
+      // ---- level-pinned bypass (BYP). While the minimum level is m, a counter with count > m
+      // is never evicted (P:82 evicts a counter with the least count) and a hit only raises it, so
+      // the hits of such a key commute with every other update of the level: they change no
+      // decision (victims are the slots at count m, in slot order) and can be counted aside. At
+      // the start of a level the launch's frequent keys (hot.cu) that are monitored with count > m
+      // are *pinned* for the level: the raw items are classified 32 at a time, occurrences of
+      // pinned keys add to hc[] and the others (cold) are queued, with their positions, for the
+      // exact rule, which takes its windows from the queue. Classification runs ahead of the
+      // exact cursor, so when a level ends (after the exact step that emptied B_m) the pinned
+      // occurrences at or after the oldest queued item are taken back, hc[] is added to the
+      // counters (now the true counts at that position), the next level and its pins are found,
+      // and classification restarts from that position. Exact for any table of keys.
+      uint32_t R = q, qh = 0, qt = 0;  // raw cursor; cold queue [qh, qt)
+      uint32_t rR = 0;                 // ring position of raw item R
+      uint32_t limR = 0;               // a classified window must end at or before this position
+      uint32_t pm0 = 0, pm1 = 0;       // pinned keys (bit = rank in the table)
+      uint32_t ps0 = 0, ps1 = 0;       // the slots of this lane's pinned keys (lane, lane + 32)
+      const uint32_t hc_addr = smem_u32(hc);
+      // table entry of x and its hash; rank of x from them (>= HOT_MAX: not in the table)
+      auto hot_hash = [&](KT x) -> uint32_t { return (uint32_t)x * hseed; };
+      auto hot_entry = [&](uint32_t ha) -> uint32_t { return __ldg(htab + (ha >> (32 - HOT_LOG))); };
+      auto hot_rank = [&](uint32_t e, uint32_t ha) -> uint32_t {
+        return __funnelshift_l(e ^ ha, e ^ ha, HOT_LOG);
+      };
+      auto is_pinned = [&](uint32_t hr) -> bool {  // bit hr of pm1:pm0, 0 for hr >= 64
+        uint32_t r;
+        asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%1, %2};\n\tshr.b64 t, t, %3;\n\t"
+            "cvt.u32.u64 %0, t;\n\t}"
+            : "=r"(r)
+            : "r"(pm0), "r"(pm1), "r"(hr));
+        return r & 1u;
+      };
+      auto raw_at = [&](uint32_t t) -> KT { return ring[(roff + t) % RING]; };
+      auto set_R = [&](uint32_t t) {
+        R = t;
+        rR = (roff + t) % RING;
+      };
+      // The window [R, R + nv) may be classified if its last stage is at most one past the stage
+      // of the oldest queued item (waiting for a stage refills the slot two stages back).
+      auto upd_lim = [&]() {
+        const uint32_t hp = qt != qh ? cqp[qh & (SS_CQ - 1)] : R;
+        limR = ((roff + hp) / ST + 2) * ST - roff;
+      };
+      // second half of a window's classification (x at lane, its table entry and hash loaded
+      // earlier): count pinned occurrences, queue the others
+      auto classify_tail = [&](KT x, uint32_t e, uint32_t ha, bool act, uint32_t nv) {
+        const uint32_t hr = hot_rank(e, ha);
+        const bool pin = act && is_pinned(hr);
+        if (pin) asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hc_addr + 4 * hr) : "memory");
+        const bool cold = act && !pin;
+        const uint32_t cm = __ballot_sync(PSS_FULL, cold);
+        const uint32_t o = (qt + __popc(cm & ltm)) & (SS_CQ - 1);
+        if (cold) {
+          cq[o] = x;
+          cqp[o] = (uint16_t)(R + lane);
+        }
+        qt += __popc(cm);
+        R += nv;
+        rR += nv;
+        if (rR >= RING) rR -= RING;
+        SS_STAT(14, 1);
+      };
+      auto ring_raw = [&](uint32_t off) -> KT {  // raw item R + off + lane (off + lane < RING)
+        const uint32_t i = rR + off + lane;
+        return ring[i < RING ? i : i - RING];
+      };
+      auto classify = [&]() {
+        const uint32_t nv = min(32u, L - R);
+        ensure(R + nv);
+        const KT x = ring_raw(0);
+        const uint32_t ha = hot_hash(x);
+        classify_tail(x, hot_entry(ha), ha, lane < nv, nv);
+        __syncwarp();
+      };
+      // a level ended (or the fill phase did): true counts at the oldest queued item, the next
+      // level, its pins; classification restarts there
+      auto level_b = [&]() {
+        if constexpr (BYP) {
+          __syncwarp();
+          const uint32_t p = qt != qh ? cqp[qh & (SS_CQ - 1)] : R;
+          for (uint32_t t0 = p; t0 < R; t0 += 32) {  // take the look-ahead back
+            const uint32_t t = t0 + lane;
+            if (t < R) {
+              const uint32_t ha = hot_hash(raw_at(t));
+              const uint32_t hr = hot_rank(hot_entry(ha), ha);
+              if (is_pinned(hr)) atomicSub(&hc[hr], 1u);
+            }
+          }
+          __syncwarp();
+          if ((pm0 >> lane) & 1u) cnt[ps0] += hc[lane];
+          if ((pm1 >> lane) & 1u) cnt[ps1] += hc[lane + 32];
+          hc[lane] = 0;
+          hc[lane + 32] = 0;
+          __syncwarp();
+          new_level();
+          int32_t s;
+          uint32_t ce, fi, fp, fbits;
+          lookup((KT)hk0, lane < nhot, s, ce, fi, fp, fbits);
+          const bool p0 = s >= 0 && (ce & CM) > m;
+          ps0 = p0 ? (uint32_t)s : 0u;
+          pm0 = __ballot_sync(PSS_FULL, p0);
+          lookup((KT)hk1, lane + 32 < nhot, s, ce, fi, fp, fbits);
+          const bool p1 = s >= 0 && (ce & CM) > m;
+          ps1 = p1 ? (uint32_t)s : 0u;
+          pm1 = __ballot_sync(PSS_FULL, p1);
+          set_R(p);
+          qt = qh;
+          upd_lim();
+        }
+      };
+      if (size == k) {
+        if (BYP && nhot)
+          level_b();
+        else
+          new_level();
+      }
 
       // ---- all k counters occupied: misses evict the lowest slots of B_m (R1)
 #ifdef PSS_STATS
@@ -571,16 +717,40 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 #endif
       // one step; F: a full 32-item window (every step but the block's last), compiled separately
       // so that the window-length predicates fold away
-      auto full_step = [&](auto full) {
+      auto full_step = [&](auto full, auto fromq) {
         constexpr bool F = decltype(full)::value;
-        const uint32_t nv = F ? 32u : min(32u, L - q);
-        ensure(q + nv);
+        constexpr bool Q = decltype(fromq)::value;  // the window is the head of the cold queue
+        const uint32_t nv = F ? 32u : (Q ? qt - qh : min(32u, L - q));
+        if constexpr (!Q) ensure(q + nv);
 #ifdef PSS_STATS
         tk = clock64();
 #endif
         const bool act = F || lane < nv;
         const uint32_t amask = F || nv >= 32 ? PSS_FULL : ((1u << nv) - 1u);
-        const KT x = ring_at(lane);
+        KT x;
+        if constexpr (Q)
+          x = cq[(qh + lane) & (SS_CQ - 1)];
+        else
+          x = ring_at(lane);
+        // bypass: up to two raw windows are classified inside a full step -- their loads are
+        // issued here, their results are consumed after the step's updates, so the
+        // classification's latencies overlap the step's dependent chain
+        bool doA = false, doB = false;
+        KT xA = 0, xB = 0;
+        uint32_t hA = 0, hB = 0, eA = 0, eB = 0;
+        if constexpr (Q && F) {
+          const uint32_t room = SS_CQ - (qt - qh);
+          const uint32_t lim = min(L, limR);
+          doA = R + 32u <= lim && room >= 32u;
+          doB = R + 64u <= lim && room >= 64u;
+          if (doA) ensure(R + (doB ? 64u : 32u));
+          xA = ring_raw(0);
+          xB = ring_raw(32);
+          hA = hot_hash(xA);
+          hB = hot_hash(xB);
+          eA = hot_entry(hA);
+          eB = hot_entry(hB);
+        }
         // the match is issued first and its result first used after the lookups, so that its
         // latency (it grows with the number of distinct keys) overlaps them
         const uint32_t grp_all = __match_any_sync(PSS_FULL, x);
@@ -675,19 +845,53 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         const uint32_t last = __shfl_sync(PSS_FULL, myvic, (Mp ? Mp : 1) - 1);
         if (Mp) cur = last + 1;
         bmcount -= __popc(__ballot_sync(PSS_FULL, hitm)) + Mp;
-        advance(c);
+        if constexpr (Q) {
+          qh += c;
+          if constexpr (F) {
+            if (doA) classify_tail(xA, eA, hA, true, 32u);
+            if (doB) classify_tail(xB, eB, hB, true, 32u);
+          }
+          __syncwarp();
+          upd_lim();
+        } else {
+          advance(c);
+        }
         SS_STAT(0, 1);
         SS_STAT(9, Mp);
         SS_STAT(1, c);
         if (bmcount == 0) {
           SS_STAT(7, 1);
-          new_level();
+          if constexpr (Q)
+            level_b();
+          else
+            new_level();
         }
         __syncwarp();
         SS_TICK(ph5, tk, bmcount);
       };
-      while (q + 32 <= L) full_step(std::true_type{});
-      while (q < L) full_step(std::false_type{});
+      if (BYP && nhot) {
+        if constexpr (BYP) {
+          while (size == k) {
+            while (qt - qh < 32u && R < L && R + min(32u, L - R) <= limR) classify();
+            upd_lim();
+            if (qt == qh) {
+              if (R >= L) break;
+              continue;  // an empty queue never blocks classification
+            }
+            if (qt - qh >= 32u)
+              full_step(std::true_type{}, std::true_type{});
+            else
+              full_step(std::false_type{}, std::true_type{});
+          }
+          // the block's end: nothing is queued or ahead, the pinned counts are final
+          if ((pm0 >> lane) & 1u) cnt[ps0] += hc[lane];
+          if ((pm1 >> lane) & 1u) cnt[ps1] += hc[lane + 32];
+          __syncwarp();
+        }
+      } else {
+        while (q + 32 <= L) full_step(std::true_type{}, std::false_type{});
+        while (q < L) full_step(std::false_type{}, std::false_type{});
+      }
 #ifdef PSS_STATS
       SS_STAT(11, ph1);
       SS_STAT(12, ph2);
@@ -720,6 +924,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
 // ------------------------------------------------------------------------------ host side
 struct SSPlan {
   bool gstate, packed;
+  bool byp;   // level-pinned bypass: u32 keys, packed counters, long blocks (or forced)
   uint32_t cb, sb, fmask;
   SSLayout L;
   size_t smem;
@@ -727,9 +932,9 @@ struct SSPlan {
   int slots;  // resident CTAs the device holds
 };
 
-template <typename KT, typename ET, bool G, bool PK>
+template <typename KT, typename ET, bool G, bool PK, bool BY = false>
 static int ss_blocks_per_sm(size_t smem, const DevInfo& d) {
-  auto kern = ss_summarize_kernel<KT, ET, G, PK>;
+  auto kern = ss_summarize_kernel<KT, ET, G, PK, 0, 0, BY>;
   if (smem > (size_t)d.smem_optin || allow_max_smem(kern, d) != cudaSuccess) return 0;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32, smem) != cudaSuccess) {
@@ -739,7 +944,15 @@ static int ss_blocks_per_sm(size_t smem, const DevInfo& d) {
   return nb;  // 0: does not fit
 }
 
-static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d) {
+// PSS_BYPASS: 0 = never use the level-pinned bypass, 2 = use it whenever the kernel supports the
+// shape and keep any table (test hook: small blocks, few hot keys); unset/1 = the default gate
+static int ss_bypass_mode() {
+  const char* s = std::getenv("PSS_BYPASS");
+  return s ? std::atoi(s) : 1;
+}
+
+static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo& d,
+                      bool want_byp = true) {
   SSPlan p;
   // count + error in one word: counts <= Lmax need cb bits, errors <= Lmax / k the rest
   const uint64_t Lmax = (n + P - 1) / P;
@@ -751,8 +964,12 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
   while ((1u << sb) - 1u < k) ++sb;
   const double dl = ss_debug_load();
   uint32_t NB = ss_buckets(k, dl > 0 ? dl : SS_LOAD);
-  SSLayout Ls = ss_layout(k, kb, 2, p.packed, NB);
+  const int bm = ss_bypass_mode();
+  p.byp = want_byp && kb == 4 && p.packed && bm != 0 && Lmax <= 65536 &&
+          (bm == 2 || (Lmax >= 8192 && k >= 128));
+  SSLayout Ls = ss_layout(k, kb, 2, p.packed, NB, p.byp);
   p.gstate = k > SS_K_SMALL || Ls.total > SS_SMEM_STATE_MAX;
+  if (p.gstate) p.byp = false;
   if (!p.gstate) {
     p.sb = sb;
     p.fmask = (1u << (16 - sb)) - 1u;
@@ -761,26 +978,33 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
       pad = (size_t)std::atoll(ps);
     auto smem_of = [&](const SSLayout& L) { return SS_RING_BYTES + SS_BAR_BYTES + L.total + pad; };
     auto blocks = [&](size_t smem) {
+      if (p.byp) return ss_blocks_per_sm<uint32_t, uint16_t, false, true, true>(smem, d);
       if (p.packed)
         return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, true>(smem, d)
                        : ss_blocks_per_sm<uint64_t, uint16_t, false, true>(smem, d);
       return kb == 4 ? ss_blocks_per_sm<uint32_t, uint16_t, false, false>(smem, d)
                      : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem, d);
     };
-    const int nb = blocks(smem_of(Ls));
+    // occupancy of the layout without the bypass arrays at the default load; the bypass keeps it
+    // by giving up index entries (down to load 0.30) rather than a warp per SM
+    int nb = blocks(smem_of(ss_layout(k, kb, 2, p.packed, NB, false)));
     // The shared memory left over at this occupancy goes to the index: the largest bucket count
     // that keeps `nb` warps per SM (fewer fingerprint collisions and serial inserts).
     if (dl == 0 && nb > 0) {
-      uint32_t lo = NB, hi = 2 * NB;
-      while (lo < hi) {
+      uint32_t lo = p.byp ? ss_buckets(k, 0.30) : NB, hi = 2 * NB;
+      const int nlo = blocks(smem_of(ss_layout(k, kb, 2, p.packed, lo, p.byp)));
+      if (nlo < nb) nb = nlo;
+      while (lo < hi && nb > 0) {
         const uint32_t mid = (lo + hi + 1) / 2;
-        if (blocks(smem_of(ss_layout(k, kb, 2, p.packed, mid))) >= nb)
+        if (blocks(smem_of(ss_layout(k, kb, 2, p.packed, mid, p.byp))) >= nb)
           lo = mid;
         else
           hi = mid - 1;
       }
       NB = lo;
-      Ls = ss_layout(k, kb, 2, p.packed, NB);
+      Ls = ss_layout(k, kb, 2, p.packed, NB, p.byp);
+    } else {
+      nb = blocks(smem_of(Ls));
     }
     p.L = Ls;
     p.smem = smem_of(Ls);
@@ -802,7 +1026,7 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
 // workspace: K1's partition queues, the histogram kernel's queues and per-leaf flags, K1's
 // global-memory states (large k)
 struct SumWs {
-  size_t q, hq, flagged, g, total;
+  size_t q, hq, flagged, hot, g, total;
 };
 static SumWs sum_ws(const SSPlan& p, uint32_t P) {
   SumWs w;
@@ -810,6 +1034,7 @@ static SumWs sum_ws(const SSPlan& p, uint32_t P) {
   w.q = b.take<uint32_t>(SS_MAX_RANGES);
   w.hq = b.take<uint32_t>(SS_MAX_RANGES);
   w.flagged = b.take<unsigned char>(P);
+  w.hot = p.byp ? b.take<uint32_t>((size_t)HOT_WORDS * SS_MAX_RANGES) : 0;
   w.g = p.gstate ? b.take<unsigned char>(p.L.total * (size_t)p.grid) : 0;
   w.total = b.bytes();
   return w;
@@ -827,7 +1052,7 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   SSPlan p = ss_plan(n, kb, k, P, d);
   if (r1 > P) r1 = P;
   if (r0 >= r1 || qi >= SS_MAX_RANGES) return cudaErrorInvalidValue;
-  const int grid = (int)std::min<uint64_t>(r1 - r0, (uint64_t)p.grid);
+  int grid = (int)std::min<uint64_t>(r1 - r0, (uint64_t)p.grid);
   const SumWs W = sum_ws(p, P);
   unsigned char* w = static_cast<unsigned char*>(ws);
   // blocks with at most k distinct keys: the histogram kernel; K1 takes the others
@@ -870,8 +1095,54 @@ cudaError_t summarize_launch(const void* A, uint64_t n, int kb, uint32_t k, uint
   a.cb = p.cb;
   a.sb = p.sb;
   a.fmask = p.fmask;
+  a.o_hc = p.L.hc;
+  a.o_cq = p.L.cq;
+  a.o_cqp = p.L.cqp;
+  a.hot = nullptr;
   cudaError_t e = cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
+  if (p.byp) {  // K0: the frequent keys of the launch's range of A (hot.cu)
+    auto bound = [&](uint64_t r) -> uint64_t {  // first item of partition r (the kernel's bounds)
+      if (T <= 1) return (uint64_t)((unsigned __int128)r * n / P);
+      const uint64_t Pp = P / T, pr = r / T, t = r % T;
+      if (pr >= Pp) return n;
+      const uint64_t b0 = pr * n / Pp, Lp = (pr + 1) * n / Pp - b0;
+      return b0 + t * Lp / T;
+    };
+    const uint64_t lo = bound(r0), hi = bound(r1);
+    uint32_t* hot = reinterpret_cast<uint32_t*>(w + W.hot) + (size_t)qi * HOT_WORDS;
+    if (hi > lo) {
+      e = hot_sample_launch(A, lo, hi, hot, ss_bypass_mode() == 2, s);
+      if (e != cudaSuccess) return e;
+      a.hot = hot;
+    }
+  }
+  if (a.hot) {
+    // Whether the range has a table is known on the device only: the bypass kernel is launched
+    // first and returns at once without one; the plain kernel (its own layout: no queue, a
+    // larger index) follows and returns at once if the bypass kernel took the range.
+    const int spec = p.cb == 17 && p.sb == 10 ? 10 : 0;
+    SumArgs ab = a;
+    ab.pdl = 0;
+    if (spec == 10) {
+      allow_max_smem(ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17, true>, d);
+      ss_summarize_kernel<uint32_t, uint16_t, false, true, 10, 17, true><<<grid, 32, p.smem, s>>>(ab);
+    } else {
+      ss_summarize_kernel<uint32_t, uint16_t, false, true, 0, 0, true><<<grid, 32, p.smem, s>>>(ab);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    p = ss_plan(n, kb, k, P, d, false);
+    grid = (int)std::min<uint64_t>(r1 - r0, (uint64_t)p.grid);
+    a.gstride = p.L.total;
+    a.o_cnt = p.L.cnt;
+    a.o_err = p.L.err;
+    a.o_pos = p.L.pos;
+    a.o_bm = p.L.bm;
+    a.o_vic = p.L.vic;
+    a.o_T = p.L.T;
+    a.NB = p.L.NB;
+  }
   if (!p.gstate) {
     if (p.packed) {
       // the common shape compiled with its layout constants: k in [512, 1023] (slot bits 10) and

@@ -67,8 +67,8 @@ def main():
     s = list(st)
     names = ["full_steps", "items", "slow_insert_lanes", "rehash", "amb_steps", "trunc_victims",
              "trunc_hazard", "new_level", "fill_steps", "evictions", "no_free_entry_lanes",
-             "refills", "lost_claim_steps", "dup_miss_steps", "unused14",
-             "unused15"]
+             "ph1_cycles", "ph2_cycles", "ph3_cycles", "classify_windows",
+             "pinned_items"]
     full = max(1, s[0])
     print(f"workload {args.workload} n={n} k={k} P={P}")
     for i, nm in enumerate(names):
