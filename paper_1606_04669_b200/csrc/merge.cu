@@ -43,6 +43,7 @@ struct CombArgs {
   size_t o_ucnt, o_uerr, o_dead, o_ht, o_x;
   uint32_t logH2;
   uint32_t NP;  // sort width
+  uint32_t no_x;  // the working set has no exchange buffer (tree kernel of large summaries)
 };
 
 struct MLayout {
@@ -285,6 +286,9 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
   constexpr int NW = NT / 32;
   __shared__ KT kres;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  // tkey == nullptr: the tied items are read through their indices (the tree kernel of large
+  // summaries keeps no tkey array and puts tl over the hash table, free by now)
+  auto tie_key = [&](uint32_t j) -> KT { return tkey ? tkey[j] : ukey[tl[j]]; };
   uint32_t live = 0, mn = 0xffffffffu, mx = 0;
   for (uint32_t i = tid; i < N; i += NT) {
     if (i >= n1 && dead[i - n1]) continue;
@@ -360,7 +364,7 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
       const uint32_t o = warp_append(&hist[259], t);
       if (t) {
         tl[o] = i;
-        tkey[o] = ukey[i];
+        if (tkey) tkey[o] = ukey[i];
       }
     }
     __syncthreads();
@@ -369,9 +373,9 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
     if (!all_eq) {
       if (E <= TIE_RANK_MAX) {  // items in the union are distinct: ranks are exact
         for (uint32_t j = tid; j < E; j += NT) {
-          const KT x = tkey[j];
+          const KT x = tie_key(j);
           uint32_t r = 0;
-          for (uint32_t u = 0; u < E; ++u) r += tkey[u] < x;
+          for (uint32_t u = 0; u < E; ++u) r += tie_key(u) < x;
           if (r == need - 1) kres = x;
         }
         __syncthreads();
@@ -383,7 +387,7 @@ __device__ void select_topk_write(uint32_t N, uint32_t n1, uint32_t k, const KT*
           uint32_t* const nxt = hb + 258 * ((pb + 1) & 1u);
           for (uint32_t b = tid; b < 256; b += NT) nxt[b] = 0;
           for (uint32_t j = tid; j < E; j += NT) {
-            const KT x = tkey[j];
+            const KT x = tie_key(j);
             if ((x & kmask) == K) atomicAdd(&cur[(uint32_t)(x >> shift) & 255u], 1u);
           }
           __syncthreads();
@@ -436,6 +440,8 @@ struct CombSmem {
   uint32_t* xhi;
   uint32_t* xidx;
   KT* xlo;
+  uint32_t* tl;  // Prune(k)'s list of counters tied at the threshold: indices, items
+  KT* tkey;
   uint32_t* red;
   uint32_t* hist;
 };
@@ -451,6 +457,8 @@ __device__ __forceinline__ CombSmem<KT> comb_smem(const CombArgs& a, unsigned ch
   m.xhi = reinterpret_cast<uint32_t*>(base + a.o_x);
   m.xidx = m.xhi + a.NP;
   m.xlo = reinterpret_cast<KT*>(m.xidx + a.NP);
+  m.tl = a.no_x ? m.ht : m.xidx;  // no exchange buffer: the hash table's space, indices only
+  m.tkey = a.no_x ? nullptr : m.xlo;
   m.red = red;
   m.hist = hist;
   return m;
@@ -588,7 +596,7 @@ __device__ void combine_node(const CombArgs& a, const NodeRef& ina, uint32_t li,
   // Prune(k) (Alg. 2 l.19): order by (count desc, item asc), keep the first k (R5)
   const uint32_t N = n1 + n2;
   if (!a.sort_out) {  // internal tree node: the top-k set
-    select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, xidx, xlo, oi, oc,
+    select_topk_write<KT, NT>(N, n1, k, ukey, ucnt, uerr, dead, hist, red, sm.tl, sm.tkey, oi, oc,
                               oe, o.sizes + blk, lv);
     if (tid == 0) {
 #ifdef PSS_MSTATS
@@ -757,6 +765,7 @@ static void fill_comb_args(CombArgs& a, int, uint32_t k, const MPlan& p, void* w
   a.o_x = p.L.x;
   a.logH2 = p.L.logH2;
   a.NP = p.L.NP;
+  a.no_x = 0;
 }
 
 template <typename KT, bool G, int NT, int EPT>
@@ -1007,9 +1016,23 @@ static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, p.smem) != cudaSuccess ||
       nb < 1)
     nb = 1;
+  // Internal nodes need the exchange buffer only for Prune(k)'s tie list. When it costs
+  // residency (k around 2000: one CTA per SM), the list goes over the hash table instead
+  // (indices only) and the buffer is dropped: 2-3 CTAs per SM.
+  size_t smem = p.smem;
+  TreeArgs tb = ta;
+  if (nb < 1536 / NT) {
+    int nb2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, kern, NT, p.L.x) == cudaSuccess &&
+        nb2 > nb) {
+      nb = nb2;
+      smem = p.L.x;
+      tb.a.no_x = 1;
+    }
+  }
   const int grid = (int)std::min<uint64_t>(ta.off[ta.nlev], (uint64_t)nb * d.sms);
   if (!ta.leaf_flags) {
-    kern<<<grid, NT, p.smem, s>>>(ta);
+    kern<<<grid, NT, smem, s>>>(tb);
     return cudaGetLastError();
   }
   // overlapping K1: a programmatic dependent launch (K1 triggers it at its start; the tree's CTAs
@@ -1017,14 +1040,14 @@ static cudaError_t launch_tree(const TreeArgs& ta, const MPlan& p, const DevInfo
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = p.smem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta);
+  return cudaLaunchKernelEx(&cfg, kern, tb);
 }
 
 bool merge_tree_overlaps(int kb, uint32_t k, uint32_t P, const DevInfo& d) {
