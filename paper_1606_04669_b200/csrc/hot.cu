@@ -4,8 +4,9 @@
 // commute with every other update until the minimum level changes; K1 counts them aside. Which
 // keys are worth that is a performance choice only (K1 stays exact for any table, also an empty or
 // a badly chosen one), so one CTA picks them from a sample:
-//   1. 32768 items (32 runs of 1024 consecutive items spread over the range; the whole range if it
-//      is shorter), 32 per thread kept in registers, are counted into a sketch of 16384 buckets;
+//   1. 8192 items (8 runs of 1024 consecutive items spread over the range; the whole range if it
+//      is shorter), 8 per thread kept in registers, are counted into a sketch of 4096 buckets
+//      (32768 items took 32 us, mostly same-address shared atomics of the heaviest keys);
 //   2. the sample items whose bucket reached a threshold are counted exactly in a small
 //      open-addressing table (64-bit entries valid|key claimed by atomicCAS, no sentinel keys);
 //   3. the (up to) 64 entries with the greatest counts (ties: smaller key) are ranked;
@@ -19,9 +20,9 @@
 
 namespace pss {
 
-constexpr uint32_t HOT_SAMPLE = 32768, HOT_RUN = 1024, HOT_NT = 1024;
+constexpr uint32_t HOT_SAMPLE = 8192, HOT_RUN = 1024, HOT_NT = 1024;
 constexpr uint32_t HOT_PER = HOT_SAMPLE / HOT_NT;  // sample items per thread
-constexpr uint32_t HOT_SK_LOG = 14, HOT_ET = 2048, HOT_LIST = 1024, HOT_TRIES = 256;
+constexpr uint32_t HOT_SK_LOG = 12, HOT_ET = 2048, HOT_LIST = 1024, HOT_TRIES = 256;
 
 __device__ __forceinline__ uint32_t hot_mix(uint32_t x) {
   uint32_t h = x * 0x85EBCA6Bu;

@@ -3,8 +3,8 @@
 
   python tools/launches.py launches.csv [N]
 
-A step starts at a launch of the leaf kernel (ss_summarize_kernel); the last step is printed with
-each launch's share of it. With N, the last N launches are printed instead. Launches that are not
+A step ends with the report kernel (result_kernel); the last step (the launches after the previous
+step's report) is printed with each launch's share of it. With N, the last N launches are printed instead. Launches that are not
 libpss kernels (torch fills etc.) are marked with '*'.
 """
 import csv
@@ -21,8 +21,8 @@ def main():
         sel = out[-int(sys.argv[2]):]
         what = f"the last {len(sel)} launches"
     else:
-        starts = [i for i, (name, _) in enumerate(out) if "ss_summarize_kernel" in name]
-        sel = out[starts[-1]:] if starts else out
+        ends = [i for i, (name, _) in enumerate(out) if "result_kernel" in name]
+        sel = out[ends[-2] + 1:ends[-1] + 1] if len(ends) >= 2 else out
         what = f"the last step ({len(sel)} launches)"
     tot = sum(v for _, v in sel)
     for name, v in sel:
