@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(H_NT) hist_kernel(const HistArgs a) {
     };
     const KT* B = A + lo;
     const bool vec = (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
+    // the next trip's 16 bytes are loaded before this trip's keys are counted (the counting is a
+    // chain of shared-memory round trips; one load in flight per thread left HBM idle)
+    uint4 pre = make_uint4(0, 0, 0, 0);
+    if (vec && tid * V + V <= L) pre = *reinterpret_cast<const uint4*>(B + tid * V);
     for (uint32_t base = 0; base < L; base += H_NT * V) {
       // Give up early on blocks whose distinct keys grow too fast to stay within k: more than
       // k sqrt(f) after a fraction f of the block (a heuristic: a block given up on wrongly is
@@ -129,7 +133,9 @@ __global__ void __launch_bounds__(H_NT) hist_kernel(const HistArgs a) {
       const uint32_t p0 = base + tid * V;
       KT x[V];
       if (vec && p0 + V <= L) {
-        const uint4 v = *reinterpret_cast<const uint4*>(B + p0);
+        const uint4 v = pre;
+        const uint32_t pn = p0 + H_NT * V;
+        if (pn + V <= L) pre = *reinterpret_cast<const uint4*>(B + pn);
         if constexpr (V == 4) {
           x[0] = v.x;
           x[1] = v.y;
