@@ -111,8 +111,6 @@ constexpr int PH_TRIES = 64;
 // 16-bit counter [word][lane]; the dummy is the upper half of word 37, above every valid code
 // (at most 74 candidates). Empty entries hold the dummy's code with low bits 0. One 32-bit
 // shared-memory load and 12 instructions per key instead of a 64-bit load and 18.
-constexpr uint32_t PH_TAG_BITS = 32 - PH_LOG;
-constexpr uint32_t PH_TAG_MASK = (1u << PH_TAG_BITS) - 1u;
 constexpr uint32_t PH_TAG_MAXC = 74;
 constexpr uint32_t PH_FDUMMY = 1024u + 37u;
 __host__ __device__ constexpr uint32_t ph_fcode(uint32_t idx) {
@@ -120,13 +118,50 @@ __host__ __device__ constexpr uint32_t ph_fcode(uint32_t idx) {
 }
 static_assert(ph_fcode(PH_TAG_MAXC - 1) < PH_FDUMMY && PH_TAG_MAXC <= PH_MAX, "tagged entry");
 static_assert((PH_FDUMMY - 1024u + 1u) * 128u <= VCW_SMALL, "tagged counters fit the small area");
+// u64 keys: the same with 64-bit entries and ha = key * (a 64-bit odd multiplier derived from the
+// 32-bit one): the low 53 bits identify the key (a 64-bit shared load instead of a 128-bit one).
+template <typename KT>
+struct VTag;
+template <>
+struct VTag<uint32_t> {
+  using TE = uint32_t;
+  static constexpr uint32_t BITS = 32 - PH_LOG;
+  __host__ __device__ static __forceinline__ TE hash(uint32_t x, uint32_t mult) { return x * mult; }
+};
+template <>
+struct VTag<uint64_t> {
+  using TE = unsigned long long;
+  static constexpr uint32_t BITS = 64 - PH_LOG;
+  __host__ __device__ static __forceinline__ TE hash(uint64_t x, uint32_t mult) {
+    return x * (((unsigned long long)mult * 0x9E3779B97F4A7C15ull) | 1ull);
+  }
+};
+// entry of the table position h for the counter code f and the hash ha / for no key
+template <typename KT>
+__device__ __forceinline__ typename VTag<KT>::TE vtag_entry(uint32_t f, uint32_t h,
+                                                            typename VTag<KT>::TE ha) {
+  using TE = typename VTag<KT>::TE;
+  return ((TE)(f ^ h) << VTag<KT>::BITS) | (ha & (((TE)1 << VTag<KT>::BITS) - 1));
+}
+// counter code of a key from its entry e and hash ha
+template <typename KT>
+__device__ __forceinline__ uint32_t vtag_code(typename VTag<KT>::TE e,
+                                              typename VTag<KT>::TE ha) {
+  const typename VTag<KT>::TE t = e ^ ha;
+  if constexpr (sizeof(KT) == 4) {
+    return min(__funnelshift_l(t, t, PH_LOG), PH_FDUMMY);
+  } else {
+    const unsigned long long v = (t << PH_LOG) | (t >> (64 - PH_LOG));
+    return (uint32_t)min(v, (unsigned long long)PH_FDUMMY);
+  }
+}
 
 static VLayout v_layout(int kb, uint32_t cap) {
   VLayout L;
   Bump b;
   L.acc = b.take<unsigned long long>(cap ? cap : 1);
   L.tab = b.take<unsigned char>(((size_t)1 << std::max(v_logT(cap), PH_LOG)) * (kb == 4 ? 8 : 16));
-  L.tab32 = b.take<uint32_t>((size_t)1 << PH_LOG);  // tagged one-probe table (u32 keys)
+  L.tab32 = b.take<unsigned long long>((size_t)1 << PH_LOG);  // tagged one-probe table
   // [0] seed, [1] logT, [2] 1 = perfect table, [3] multiplier of the tagged table (0 = none)
   L.ctl = b.take<uint32_t>(4);
   L.total = b.bytes();
@@ -162,8 +197,10 @@ __device__ __forceinline__ uint32_t vlookup(const typename VEnt<KT>::T* tab, KT 
 template <typename KT>
 __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t* d_n,
                                     unsigned long long* acc, typename VEnt<KT>::T* tab,
-                                    uint32_t* tab32, uint32_t* ctl) {
+                                    void* tab32v, uint32_t* ctl) {
   using VT = typename VEnt<KT>::T;
+  using TE = typename VTag<KT>::TE;
+  TE* const tab32 = static_cast<TE*>(tab32v);
   const uint32_t nc = eff_count(cap, d_n);
   for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) acc[j] = 0;
   // perfect table: find a seed under which the (distinct) candidates occupy distinct entries
@@ -193,27 +230,27 @@ __global__ void verify_setup_kernel(const KT* cand, uint32_t cap, const uint32_t
           ctl[2] = 1;
           ctl[3] = 0;
         }
-        // the tagged table (u32 keys): its own multiplier search; ctl[3] = multiplier, 0 = none
-        if (sizeof(KT) == 4 && nc <= PH_TAG_MAXC) {
+        // the tagged table: its own multiplier search; ctl[3] = multiplier, 0 = none
+        if (nc <= PH_TAG_MAXC) {
           for (int t2 = 0; t2 < PH_TRIES; ++t2) {
             const uint32_t mult = ((uint32_t)t2 * 0x9E3779B9u + 0x85EBCA6Bu) | 1u;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < TP / 32; i += blockDim.x) occ[i] = 0;
             if (threadIdx.x == 0) clash = 0;
             __syncthreads();
-            uint32_t ha = 0, hh = 0;
+            TE ha = 0;
+            uint32_t hh = 0;
             if (threadIdx.x < nc) {
-              ha = (uint32_t)cand[threadIdx.x] * mult;
-              hh = ha >> PH_TAG_BITS;
+              ha = VTag<KT>::hash(cand[threadIdx.x], mult);
+              hh = (uint32_t)(ha >> VTag<KT>::BITS);
               if (atomicOr(&occ[hh >> 5], 1u << (hh & 31)) & (1u << (hh & 31))) clash = 1;
             }
             __syncthreads();
             if (clash) continue;
             for (uint32_t e = threadIdx.x; e < TP; e += blockDim.x)
-              tab32[e] = (PH_FDUMMY ^ e) << PH_TAG_BITS;
+              tab32[e] = vtag_entry<KT>(PH_FDUMMY, e, 0);
             __syncthreads();
-            if (threadIdx.x < nc)
-              tab32[hh] = ((ph_fcode(threadIdx.x) ^ hh) << PH_TAG_BITS) | (ha & PH_TAG_MASK);
+            if (threadIdx.x < nc) tab32[hh] = vtag_entry<KT>(ph_fcode(threadIdx.x), hh, ha);
             if (threadIdx.x == 0) ctl[3] = mult;
             break;
           }
@@ -307,10 +344,11 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
   };
 #else
   auto look = [&](KT x) -> uint32_t {
-    if constexpr (TAG) {  // tagged 32-bit entries: the counter code, PH_FDUMMY for no candidate
-      const uint32_t ha = (uint32_t)x * seed;  // seed = the table's multiplier
-      const uint32_t e = reinterpret_cast<const uint32_t*>(tab)[ha >> PH_TAG_BITS];
-      return min(__funnelshift_l(e ^ ha, e ^ ha, PH_LOG), PH_FDUMMY);
+    if constexpr (TAG) {  // tagged entries: the counter code, PH_FDUMMY for no candidate
+      using TE = typename VTag<KT>::TE;
+      const TE ha = VTag<KT>::hash(x, seed);  // seed = the table's multiplier
+      const TE e = reinterpret_cast<const TE*>(tab)[(uint32_t)(ha >> VTag<KT>::BITS)];
+      return vtag_code<KT>(e, ha);
     } else {
       return vlookup<KT>(tab, x, seed, logT, PERF);
     }
@@ -420,11 +458,12 @@ __device__ __forceinline__ void verify_scan(const KT* __restrict__ A, uint64_t n
 // sit in a one-probe table (perf) and fit per-lane counters; everything else goes to VCW_BIG.
 template <typename KT, uint32_t VCW>
 struct VKern {
-  static constexpr bool TAG = VCW == VCW_SMALL && sizeof(KT) == 4;
+  static constexpr bool TAG = VCW == VCW_SMALL;
   static constexpr size_t TAB_BYTES =
-      TAG ? ((size_t)4 << PH_LOG) : (size_t)VT_SMEM * sizeof(typename VEnt<KT>::T);
+      TAG ? (sizeof(typename VTag<KT>::TE) << PH_LOG) : (size_t)VT_SMEM * sizeof(typename VEnt<KT>::T);
   static constexpr size_t SMEM = TAB_BYTES + (size_t)VWARPS * VCW + (TAG ? PSS_VT_TAGPAD : 0);
-  static constexpr int MINB = TAG ? PSS_VT_TAGMINB : 1;  // CTAs per SM the registers must allow
+  // CTAs per SM the registers must allow
+  static constexpr int MINB = TAG ? (sizeof(KT) == 4 ? PSS_VT_TAGMINB : 6) : 1;
 };
 
 template <typename KT, uint32_t VCW>
@@ -432,7 +471,7 @@ __global__ void __launch_bounds__(VTHREADS, VKern<KT, VCW>::MINB) verify_kernel(
                                                           uint32_t cap, const uint32_t* d_n,
                                                           unsigned long long* acc,
                                                           const typename VEnt<KT>::T* gtab,
-                                                          const uint32_t* gtab32,
+                                                          const void* gtab32v,
                                                           const uint32_t* ctl, uint32_t lane_ok) {
   using VT = typename VEnt<KT>::T;
   constexpr bool TAG = VKern<KT, VCW>::TAG;
@@ -444,9 +483,7 @@ __global__ void __launch_bounds__(VTHREADS, VKern<KT, VCW>::MINB) verify_kernel(
   const uint32_t T = 1u << logT;
   const uint32_t warp = threadIdx.x >> 5;
   // counting mode (uniform): 0 per-lane u16, 1 per-warp u32 + match, 2 global + match
-  const bool small_fits =
-      sizeof(KT) == 4 ? lane_ok && perf && ctl[3] != 0 && nc <= PH_TAG_MAXC
-                      : lane_ok && nc < vlane_max(VCW_SMALL) && T <= VT_SMEM;
+  const bool small_fits = lane_ok && perf && ctl[3] != 0 && nc <= PH_TAG_MAXC;
   if (small_fits != (VCW == VCW_SMALL)) return;  // the other kernel's case
   const int mode = (lane_ok && nc < vlane_max(VCW) && T <= VT_SMEM) ? 0
                    : (nc <= vwarp_max(VCW) ? 1 : 2);
@@ -458,8 +495,9 @@ __global__ void __launch_bounds__(VTHREADS, VKern<KT, VCW>::MINB) verify_kernel(
   uint32_t* wc = reinterpret_cast<uint32_t*>(carea) + (size_t)warp * nc;        // [cand]
   const bool tab_smem = T <= VT_SMEM;
   if (TAG) {
+    using TE = typename VTag<KT>::TE;
     for (uint32_t h = threadIdx.x; h < (1u << PH_LOG); h += VTHREADS)
-      reinterpret_cast<uint32_t*>(vsm)[h] = gtab32[h];
+      reinterpret_cast<TE*>(vsm)[h] = static_cast<const TE*>(gtab32v)[h];
   } else
   if (tab_smem)
     for (uint32_t h = threadIdx.x; h < T; h += VTHREADS) stab[h] = gtab[h];
@@ -541,7 +579,7 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
   auto* acc = reinterpret_cast<unsigned long long*>(w + L.acc);
   auto* tab = reinterpret_cast<VT*>(w + L.tab);
   auto* ctl = reinterpret_cast<uint32_t*>(w + L.ctl);
-  auto* tab32 = reinterpret_cast<uint32_t*>(w + L.tab32);
+  void* tab32 = w + L.tab32;
   if (cap == 0) return cudaSuccess;
   verify_setup_kernel<KT><<<1, 1024, 0, s>>>(cand, cap, d_n, acc, tab, tab32, ctl);
   // per-lane 16-bit counters cannot overflow: a lane counts at most n / (CTAs * VTHREADS) + the
@@ -565,10 +603,9 @@ static cudaError_t verify_run(const KT* A, uint64_t n, const KT* cand, uint32_t 
     kern<<<grid, VTHREADS, smem, s>>>(A, n, cap, d_n, acc, tab, tab32, ctl, lane_ok);
   };
   launch(verify_kernel<KT, VCW_SMALL>, VKern<KT, VCW_SMALL>::SMEM);
-  // u32: the small kernel takes one-probe tables only, so the general one is always launched
+  // the small kernel takes tagged one-probe tables only, so the general one is always launched
   // (it exits at once when the case is the small kernel's)
-  if (cap >= vlane_max(VCW_SMALL) || sizeof(KT) == 4)
-    launch(verify_kernel<KT, VCW_BIG>, VKern<KT, VCW_BIG>::SMEM);
+  launch(verify_kernel<KT, VCW_BIG>, VKern<KT, VCW_BIG>::SMEM);
   verify_finalize_kernel<KT><<<(cap + 255) / 256, 256, 0, s>>>(cand, cap, d_n, acc, tab, ctl, exact);
   return cudaGetLastError();
 }
