@@ -20,6 +20,8 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import torch
 
 from . import (KEY_U32, OP_MERGE_WIDE, OP_SUMMARIZE_MERGE, OP_VERIFY, Summaries, _key_dtype,
@@ -131,8 +133,15 @@ class Runner:
         # when k allows more, the general scan, finalize), report
         top_levels = (world - 1).bit_length() if world > 1 else 0
         hist = 1 if 40 * k >= -(-n // P) and -(-n // P) <= (1 << 17) else 0
-        verify = 3 + (1 if k >= 76 else 0)
-        self.launches_per_step = (1 + hist + _merge_launches(P, k, kb) +
+        # the frequent-key sample K0 and the bypass kernel K1b in front of K1 (csrc/summarize.cu,
+        # ss_plan: u32 keys, packed counters, blocks of 2^13..2^16 keys, 128 <= k <= 4094)
+        lmax = -(-n // P)
+        cb = max(1, lmax.bit_length())
+        packed = cb < 30 and lmax // k < (1 << (30 - cb))
+        bypass = 2 if (kb == 4 and packed and 8192 <= lmax <= 65536 and 128 <= k <= 4094 and
+                       os.environ.get("PSS_BYPASS", "1") != "0") else 0
+        verify = 4  # setup, the tagged scan, the general scan (one of the two returns), finalize
+        self.launches_per_step = (1 + hist + bypass + _merge_launches(P, k, kb) +
                                   (1 + top_levels if world > 1 else 0) + 1 + verify + 1)
         self.host_api = "pss_query_host" if world == 1 else "H2D copy + step + D2H (torch)"
         self._kb = kb
