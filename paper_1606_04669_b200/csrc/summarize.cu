@@ -1016,8 +1016,14 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     p.fmask = 0xffffffffu;
     p.L = ss_layout(k, kb, 8, false, ss_buckets(k, dl > 0 ? dl : 0.32));
     p.smem = SS_RING_BYTES + SS_BAR_BYTES;
-    p.grid = (int)std::min<uint64_t>(P, (uint64_t)8 * d.sms);
-    p.slots = 8 * d.sms;
+    // Warps per SM of the global-state kernel. It is bound by the latency of its L2/DRAM accesses
+    // (IPC 0.68 at 8 warps per SM), so it takes all 32 CTA slots of an SM (C4-k5000 without K1h:
+    // 8.6 -> 3.6 ms, C4-k20000 9.5 -> 4.0 ms) as long as the states fit a 4 GiB workspace.
+    const uint64_t budget = 4ull << 30;
+    int gw = (int)std::min<uint64_t>(32, std::max<uint64_t>(8, budget / (p.L.total * (uint64_t)d.sms)));
+    if (const char* gs = std::getenv("PSS_DEBUG_GSTATE_WARPS")) gw = std::max(1, std::atoi(gs));
+    p.grid = (int)std::min<uint64_t>(P, (uint64_t)gw * d.sms);
+    p.slots = gw * d.sms;
   }
   if (p.grid < 1) p.grid = 1;
   return p;
