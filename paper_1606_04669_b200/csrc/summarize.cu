@@ -78,6 +78,18 @@ constexpr uint32_t SS_NSTAGE = PSS_SS_NSTAGE;
 constexpr uint32_t SS_STAGE_BYTES = PSS_SS_STAGE_BYTES;
 constexpr uint32_t SS_BAR_BYTES = 32;  // the ring's mbarriers (3 x 8 bytes)
 constexpr uint32_t SS_RING_BYTES = SS_NSTAGE * SS_STAGE_BYTES;
+// the bypass kernel's ring: 6 stages of which 4 stay resident behind the newest one waited for
+// (its classification runs up to 3 stages ahead of the oldest queued item), 2 in flight
+#ifndef PSS_SS_BYP_NSTAGE
+#define PSS_SS_BYP_NSTAGE 6
+#endif
+#ifndef PSS_SS_BYP_KEEP
+#define PSS_SS_BYP_KEEP 4
+#endif
+constexpr uint32_t SS_BYP_NSTAGE = PSS_SS_BYP_NSTAGE, SS_BYP_KEEP = PSS_SS_BYP_KEEP;
+constexpr uint32_t SS_BYP_RING_BYTES = SS_BYP_NSTAGE * SS_STAGE_BYTES;
+constexpr uint32_t SS_BYP_BAR_BYTES = 64;
+static_assert(SS_BYP_NSTAGE * 8 <= SS_BYP_BAR_BYTES && SS_BYP_KEEP >= 2 && SS_BYP_KEEP < SS_BYP_NSTAGE, "ring");
 constexpr size_t SS_SMEM_STATE_MAX = 100 * 1024;  // bigger per-warp state lives in global memory
 constexpr uint32_t SS_K_SMALL = 4094;             // 16-bit index entries up to this k
 constexpr double SS_LOAD = 0.24;  // index load factor (live keys / entries), before the slack fill
@@ -231,14 +243,19 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   const uint32_t lane = threadIdx.x;
   const uint32_t ltm = lanemask_lt();
   constexpr uint32_t ST = SS_STAGE_BYTES / sizeof(KT);  // items per stage
-  constexpr uint32_t RING = SS_NSTAGE * ST;  // ring capacity in items
+  // ring: NST stages, KEEP of them resident up to the newest one waited for, NST - KEEP in flight
+  constexpr uint32_t NST = BYP ? SS_BYP_NSTAGE : SS_NSTAGE, KEEP = BYP ? SS_BYP_KEEP : 2u;
+  constexpr uint32_t NFL = NST - KEEP;
+  constexpr uint32_t RING_BYTES = BYP ? SS_BYP_RING_BYTES : SS_RING_BYTES;
+  constexpr uint32_t BAR_BYTES = BYP ? SS_BYP_BAR_BYTES : SS_BAR_BYTES;
+  constexpr uint32_t RING = NST * ST;  // ring capacity in items
   constexpr uint32_t E = 16 / sizeof(KT);  // items per 16 bytes
   constexpr ET EMPTY = Ent<ET>::EMPTY;
   const Ent<ET> en{SB ? (uint32_t)SB : a.sb, SB ? (1u << (16 - SB)) - 1u : a.fmask};
 
   KT* ring = reinterpret_cast<KT*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SS_RING_BYTES);
-  unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + SS_RING_BYTES + SS_BAR_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  unsigned char* st = GSTATE ? a.gstate + (size_t)blockIdx.x * a.gstride : smem + RING_BYTES + BAR_BYTES;
   KT* keys = reinterpret_cast<KT*>(st);
   // count; if PACKED also err << cb and the index position of the slot's entry in bits 30-31
   uint32_t* cnt = reinterpret_cast<uint32_t*>(st + a.o_cnt);
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
   const uint64_t nfloor = aligned ? (n & ~(uint64_t)(E - 1)) : 0;
 
   if (lane == 0) {
-    for (uint32_t j = 0; j < SS_NSTAGE; ++j) mbar_init(&bars[j], 1);
+    for (uint32_t j = 0; j < NST; ++j) mbar_init(&bars[j], 1);
     fence_mbar_init();
   }
   for (uint32_t i = kw + lane; i < kw + 2; i += 32) bm[i] = 0;  // guard words
@@ -443,9 +460,9 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         }
         for (uint64_t t = be + lane; t < b0; t += 32) dst[t - a0] = A[t];  // unaligned tail
       };
-      // stages 0..NSTAGE-2 in flight; waiting for stage g frees the slot of stage g-2 (a window
+      // stages 0..NFL in flight; waiting for stage g frees the slot of stage g-KEEP (a window
       // spans at most two stages), which is refilled with stage g+NSTAGE-2
-      for (uint32_t g = 0; g < min(total, SS_NSTAGE - 1); ++g) issue(g, g);
+      for (uint32_t g = 0; g < min(total, NFL + 1); ++g) issue(g, g);
       uint32_t ready = 0;      // stages waited for
       uint32_t rsl = 0;        // ring slot of stage `ready`
       uint32_t ready_end = 0;  // items of the partition available in the ring: [0, ready_end)
@@ -455,13 +472,13 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
           while (end > ready_end) {
             mbar_wait(&bars[rsl], (phasebits >> rsl) & 1u);
             phasebits ^= 1u << rsl;
-            // stage ready + NSTAGE - 2 goes into the slot of stage ready - 2 (consumed)
-            const uint32_t nx = ready + SS_NSTAGE - 2;
-            uint32_t nsl = rsl + SS_NSTAGE - 2;
-            if (nsl >= SS_NSTAGE) nsl -= SS_NSTAGE;
-            if (nx >= SS_NSTAGE - 1 && nx < total) issue(nx, nsl);
+            // stage ready + NFL goes into the slot of stage ready - KEEP (consumed)
+            const uint32_t nx = ready + NFL;
+            uint32_t nsl = rsl + NFL;
+            if (nsl >= NST) nsl -= NST;
+            if (nx >= NFL + 1 && nx < total) issue(nx, nsl);
             ++ready;
-            rsl = rsl + 1 == SS_NSTAGE ? 0u : rsl + 1;
+            rsl = rsl + 1 == NST ? 0u : rsl + 1;
             ready_end = min(L, ready * ST - roff);
           }
           __syncwarp();
@@ -632,10 +649,10 @@ __global__ void __launch_bounds__(32) ss_summarize_kernel(const SumArgs a) {
         rR = (roff + t) % RING;
       };
       // The window [R, R + nv) may be classified if its last stage is at most one past the stage
-      // of the oldest queued item (waiting for a stage refills the slot two stages back).
+      // of the oldest queued item (waiting for a stage refills the slot KEEP stages back).
       auto upd_lim = [&]() {
         const uint32_t hp = qt != qh ? cqp[qh & (SS_CQ - 1)] : R;
-        limR = ((roff + hp) / ST + 2) * ST - roff;
+        limR = ((roff + hp) / ST + KEEP) * ST - roff;
       };
       // second half of a window's classification (x at lane, its table entry and hash loaded
       // earlier): count pinned occurrences, queue the others
@@ -976,7 +993,8 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
     size_t pad = 0;
     if (const char* ps = std::getenv("PSS_DEBUG_SMEM_PAD"))  // experiment hook: fewer warps/SM
       pad = (size_t)std::atoll(ps);
-    auto smem_of = [&](const SSLayout& L) { return SS_RING_BYTES + SS_BAR_BYTES + L.total + pad; };
+    const size_t ringb = p.byp ? SS_BYP_RING_BYTES + SS_BYP_BAR_BYTES : SS_RING_BYTES + SS_BAR_BYTES;
+    auto smem_of = [&](const SSLayout& L) { return ringb + L.total + pad; };
     auto blocks = [&](size_t smem) {
       if (p.byp) return ss_blocks_per_sm<uint32_t, uint16_t, false, true, true>(smem, d);
       if (p.packed)
@@ -986,12 +1004,12 @@ static SSPlan ss_plan(uint64_t n, int kb, uint32_t k, uint32_t P, const DevInfo&
                      : ss_blocks_per_sm<uint64_t, uint16_t, false, false>(smem, d);
     };
     // occupancy of the layout without the bypass arrays at the default load; the bypass keeps it
-    // by giving up index entries (down to load 0.30) rather than a warp per SM
-    int nb = blocks(smem_of(ss_layout(k, kb, 2, p.packed, NB, false)));
+    // by giving up index entries (down to load 0.36) rather than a warp per SM
+    int nb = blocks(SS_RING_BYTES + SS_BAR_BYTES + ss_layout(k, kb, 2, p.packed, NB, false).total + pad);
     // The shared memory left over at this occupancy goes to the index: the largest bucket count
     // that keeps `nb` warps per SM (fewer fingerprint collisions and serial inserts).
     if (dl == 0 && nb > 0) {
-      uint32_t lo = p.byp ? ss_buckets(k, 0.30) : NB, hi = 2 * NB;
+      uint32_t lo = p.byp ? ss_buckets(k, 0.36) : NB, hi = 2 * NB;
       const int nlo = blocks(smem_of(ss_layout(k, kb, 2, p.packed, lo, p.byp)));
       if (nlo < nb) nb = nlo;
       while (lo < hi && nb > 0) {
