@@ -123,11 +123,15 @@ __global__ void __launch_bounds__(H_NT) hist_kernel(const HistArgs a) {
     if (vec && tid * V + V <= L) pre = *reinterpret_cast<const uint4*>(B + tid * V);
     for (uint32_t base = 0; base < L; base += H_NT * V) {
       // Give up early on blocks whose distinct keys grow too fast to stay within k: more than
-      // k sqrt(f) after a fraction f of the block (a heuristic: a block given up on wrongly is
+      // k sqrt(f) after a fraction f of the block (heuristics: a block given up on wrongly is
       // still summarized exactly, by K1)
       if (tid == 0 && base) {
         const uint64_t dd = ldv(sc);
         if (dd * dd * L > (uint64_t)a.k * a.k * base) sc[1] = 1;
+        // Zipf streams around s = 1.5 grow like f^(1/s): from 1/8 of the block on, also give up
+        // if the count extrapolated with exponent 0.6 exceeds k (C3-s1.5: given up at 1/8 instead
+        // of 1/2 of the block)
+        if (base * 8 >= L && (float)dd * __powf((float)L / (float)base, 0.6f) > (float)a.k) sc[1] = 1;
       }
       if (ldv(sc + 1)) break;
       const uint32_t p0 = base + tid * V;
