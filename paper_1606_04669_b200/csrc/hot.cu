@@ -156,13 +156,10 @@ __global__ void __launch_bounds__(HOT_NT) hot_sample_kernel(const uint32_t* __re
 cudaError_t hot_sample_launch(const void* A, uint64_t lo, uint64_t hi, uint32_t* out, bool force,
                               cudaStream_t s) {
   const size_t smem = ((size_t)4 << HOT_SK_LOG) + (size_t)HOT_ET * 12;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(hot_sample_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // per device and process-wide: set on every call (cheap), never cached per process
+  cudaError_t e = cudaFuncSetAttribute(hot_sample_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   hot_sample_kernel<<<1, HOT_NT, smem, s>>>(static_cast<const uint32_t*>(A), lo, hi, out,
                                            force ? 1u : 0u);
   return cudaGetLastError();

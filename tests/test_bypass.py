@@ -96,3 +96,20 @@ def test_same_bits_without_the_bypass(pss, monkeypatch):
     ref = oracle.leaves(A, 1000, 32, threads=8)
     for r in range(32):
         assert a.host(r) == ref[r].as_tuples(), f"leaf {r}"
+
+
+def test_other_entry_points_with_the_bypass(pss):
+    """The hybrid decomposition (two-level block bounds), the on-line stream (launches over
+    ranges of a batch) and the host-fed query (one launch per landed chunk) sample their own range
+    of A; all bit-exact with the bypass forced."""
+    from test_hybrid import test_hybrid_parity
+    from test_stream import feed_and_check
+    test_hybrid_parity(pss, 120_000, 64, 3, 8, 1.5, 1e5)
+    test_hybrid_parity(pss, 200_000, 1000, 4, 6, 1.1, 1e8)
+    A = inputs.zipf(300_000, 1.4, 1e6, seed=21)
+    feed_and_check(pss, A, 100, 4096, 8, [0, 5000, 5001, 70_000, 200_000, 300_000])
+    feed_and_check(pss, A, 100, 4096, 4, [0, 123_457, 300_000], host=True)
+    ref = oracle.pipeline(A, 100, 16, threads=8)
+    items, counts = pss.pss_query_host(torch.from_numpy(A).pin_memory(), 100, 16)
+    assert items.numpy().astype(np.uint64).tolist() == ref.result[0].tolist()
+    assert counts.numpy().astype(np.uint64).tolist() == ref.result[1].tolist()
