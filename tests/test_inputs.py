@@ -78,3 +78,22 @@ def test_ranges_of_the_stream():
     a = inputs.zipf(50_000, 1.1, 1e8, seed=2)
     b = inputs.zipf(20_000, 1.1, 1e8, seed=2, start=30_000, threads=3)
     assert np.array_equal(a[30_000:], b)
+
+
+def test_bench_custom_workload_flags():
+    """bench.py's --n/--k/--P/--zipf-s/--universe/--seed override the named workload's fields."""
+    import argparse
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "_bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    base = dict(workload="H", n=0, k=0, P=0, zipf_s=0.0, universe=0.0, seed=-1)
+    w = bench.workload_of(argparse.Namespace(**base))
+    assert (w.name, w.n, w.k, w.P) == ("H", 1 << 29, 1000, 8192)
+    w = bench.workload_of(argparse.Namespace(**{**base, "P": 4096}))
+    assert (w.name, w.P) == ("H", 4096)
+    w = bench.workload_of(argparse.Namespace(**{**base, "n": 10**6, "k": 50, "zipf_s": 1.3, "seed": 7}))
+    assert (w.name, w.n, w.k, w.s, w.seed, w.universe) == ("H-custom", 10**6, 50, 1.3, 7, 1e8)
+    assert bench.l2_flush_needed(w) and not bench.l2_flush_needed(bench.workload_of(argparse.Namespace(**base)))
